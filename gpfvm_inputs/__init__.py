@@ -1,0 +1,209 @@
+"""Seeded synthetic inputs shared by the oracle (``oracle/``) and the CUDA path.
+
+This module holds *problem descriptions only*: grids of finite-volume cells,
+IC/BC observation sites, PDE operator coefficients, observation noise levels,
+right-hand sides computed from the analytic initial conditions, prediction
+grids and seeded random vectors.  It contains none of the method's arithmetic
+(no kernel evaluation, no Gram assembly, no solves), so that ``oracle/`` and
+``paper_2406_05020_b200/`` can both consume it without sharing code
+(DESIGN.md §3 "independence").
+
+Notation follows PAPER.md:
+  * a block of observations is a *factorized scheme* (PAPER.md l.306-313,
+    §4 Definition): per dimension a list of 1D sites, the block's observations
+    are the Cartesian product, flattened row-major (dimension 0 = time slowest);
+  * every observation of a block is the functional
+    ``sum_tau c_tau  prod_i L_{site_i; alpha_tau,i}`` (Eq. 15-16,
+    l.244-246) where a site is an interval [a,b] (FVM cell, the functional is
+    int_a^b d^m/dx^m) or a point p (u^{(m)}(p), collocation/IC/BC functionals,
+    PAPER.md l.170);
+  * ``output`` selects the output of a multi-output prior (Eq. 17-19).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+POINT = 0
+INTERVAL = 1
+
+
+@dataclass
+class Kernel1D:
+    """Half-integer Matérn factor nu = q + 1/2 (Eq. 12, l.215)."""
+    q: int
+    lengthscale: float
+    variance: float = 1.0
+
+
+@dataclass
+class Sites:
+    """1D site list of one dimension of one block (all sites of one kind)."""
+    kind: int                 # POINT or INTERVAL
+    lo: np.ndarray            # interval left end, or the point location
+    hi: np.ndarray            # interval right end (== lo for points)
+
+    @property
+    def n(self) -> int:
+        return int(self.lo.shape[0])
+
+
+@dataclass
+class Term:
+    """One term c * D^alpha [u_output] of the (linear) operator of a block."""
+    coeff: float
+    order: Tuple[int, ...]
+    output: int = 0
+
+
+@dataclass
+class Block:
+    name: str
+    sites: List[Sites]
+    terms: List[Term]
+    noise: float              # observation noise variance Sigma_jj
+    deflate: bool             # True: IC/BC block solved exactly (§4.2)
+    rhs: np.ndarray           # observed values y for this block (flattened)
+
+    @property
+    def shape(self) -> Tuple[int, ...]:
+        return tuple(s.n for s in self.sites)
+
+    @property
+    def size(self) -> int:
+        return int(np.prod(self.shape))
+
+
+@dataclass
+class Problem:
+    name: str
+    ndim: int
+    kernels: List[List[Kernel1D]]     # [output][dim]
+    blocks: List[Block]
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_outputs(self) -> int:
+        return len(self.kernels)
+
+    @property
+    def size(self) -> int:
+        return sum(b.size for b in self.blocks)
+
+    @property
+    def offsets(self) -> List[int]:
+        off = [0]
+        for b in self.blocks:
+            off.append(off[-1] + b.size)
+        return off
+
+    def rhs(self) -> np.ndarray:
+        return np.concatenate([b.rhs for b in self.blocks]).astype(np.float64)
+
+
+@dataclass
+class Grid:
+    """Tensor prediction grid: the Cartesian product of per-dimension points."""
+    points: List[np.ndarray]
+    output: int = 0
+
+    @property
+    def shape(self) -> Tuple[int, ...]:
+        return tuple(len(p) for p in self.points)
+
+
+def cells(n: int, lo: float = 0.0, hi: float = 1.0) -> Sites:
+    """n uniform cells of [lo, hi] (FVM volumes that "disjointly span the
+    entire domain")."""
+    e = np.linspace(lo, hi, n + 1)
+    return Sites(INTERVAL, e[:-1].copy(), e[1:].copy())
+
+
+def point(p: float) -> Sites:
+    return Sites(POINT, np.array([p], dtype=np.float64), np.array([p], dtype=np.float64))
+
+
+def points(ps: Sequence[float]) -> Sites:
+    a = np.asarray(ps, dtype=np.float64)
+    return Sites(POINT, a.copy(), a.copy())
+
+
+# ---------------------------------------------------------------------------
+# 1D heat equation u_t = kappa u_xx on [0,1]x[0,1] (BASELINE.json configs 0, 1)
+# ---------------------------------------------------------------------------
+
+def sine_series_ic(n_modes: int, seed: int) -> np.ndarray:
+    """Amplitudes A_k ~ N(0, 1/k^2), k = 1..n_modes (BASELINE.json config 1)."""
+    rng = np.random.default_rng(seed)
+    k = np.arange(1, n_modes + 1)
+    return rng.standard_normal(n_modes) / k
+
+
+def heat_analytic(amps: np.ndarray, kappa: float, t: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """u(t,x) = sum_k A_k exp(-kappa k^2 pi^2 t) sin(k pi x): the separation-
+    of-variables solution of u_t = kappa u_xx with u(t,0)=u(t,1)=0."""
+    k = np.arange(1, len(amps) + 1)
+    tt = np.asarray(t, dtype=np.float64)[:, None, None]
+    xx = np.asarray(x, dtype=np.float64)[None, :, None]
+    return np.sum(amps * np.exp(-kappa * (k * np.pi) ** 2 * tt) * np.sin(k * np.pi * xx), axis=-1)
+
+
+def heat_problem(nt: int, nx: int, *, kappa: float = 0.1, ell_t: float = 0.5, ell_x: float = 0.2,
+                 q: int = 2, amps: np.ndarray | None = None, jitter: float = 1e-8,
+                 pde_noise: float = 0.0, name: str | None = None) -> Problem:
+    """FVM problem for u_t - kappa u_xx = 0 with IC u(0,x) = sum_k A_k sin(k pi x)
+    and Dirichlet-0 BC.
+
+    Blocks (in this order):
+      IC   : t = point 0,     x = nx cells, functional  int_cell u(0,x) dx
+      BC0  : t = nt cells,    x = point 0,  functional  int_cell u(t,0) dt
+      BC1  : t = nt cells,    x = point 1,  functional  int_cell u(t,1) dt
+      PDE  : t = nt cells,    x = nx cells, functional  int_V (u_t - kappa u_xx)
+    IC/BC observation noise: ``jitter * h^2`` with h the cell width (the
+    prior variance of a cell integral of a unit-variance process is ~h^2);
+    DESIGN.md reading R4.
+    """
+    if amps is None:
+        amps = np.array([1.0])
+    T = cells(nt)
+    X = cells(nx)
+    ht, hx = 1.0 / nt, 1.0 / nx
+    k = np.arange(1, len(amps) + 1)
+    a, b = X.lo, X.hi
+    ic = np.sum(amps[None, :] * (np.cos(k[None, :] * np.pi * a[:, None]) -
+                                  np.cos(k[None, :] * np.pi * b[:, None])) / (k[None, :] * np.pi), axis=1)
+    blocks = [
+        Block("IC", [point(0.0), X], [Term(1.0, (0, 0))], jitter * hx * hx, True, ic),
+        Block("BC0", [T, point(0.0)], [Term(1.0, (0, 0))], jitter * ht * ht, True, np.zeros(nt)),
+        Block("BC1", [T, point(1.0)], [Term(1.0, (0, 0))], jitter * ht * ht, True, np.zeros(nt)),
+        Block("PDE", [T, X], [Term(1.0, (1, 0)), Term(-kappa, (0, 2))], pde_noise, False,
+              np.zeros(nt * nx)),
+    ]
+    kern = [[Kernel1D(q, ell_t, 1.0), Kernel1D(q, ell_x, 1.0)]]
+    return Problem(name or f"heat1d_{nt}x{nx}", 2, kern, blocks,
+                   meta=dict(kind="heat1d", kappa=kappa, amps=np.asarray(amps), nt=nt, nx=nx))
+
+
+def config0() -> Problem:
+    """BASELINE.json configs[0]: 16x16 cells, u0 = sin(pi x), Matérn-5/2,
+    l_t = 0.5, l_x = 0.2, sigma = 1."""
+    return heat_problem(16, 16, amps=np.array([1.0]), name="config0_heat1d_16x16")
+
+
+def config1(seed: int = 1) -> Problem:
+    """BASELINE.json configs[1]: 256 time x 512 space cells, IC = seeded sum
+    of 8 sines with A_k ~ N(0, 1/k^2)."""
+    return heat_problem(256, 512, amps=sine_series_ic(8, seed), name="config1_heat1d_256x512")
+
+
+def heat_grid(nt: int, nx: int) -> Grid:
+    """Dense prediction grid on [0,1]^2 (64x64 for config 0, 512x1024 for config 1)."""
+    return Grid([np.linspace(0.0, 1.0, nt), np.linspace(0.0, 1.0, nx)], 0)
+
+
+def random_vectors(n: int, nrhs: int, seed: int) -> np.ndarray:
+    """Seeded standard-normal block of vectors, shape (nrhs, n)."""
+    return np.random.default_rng(seed).standard_normal((nrhs, n))
