@@ -1,0 +1,207 @@
+/*
+ * gpfvm.h — C ABI of the B200-native GP-FVM hot path (libgpfvm.so).
+ *
+ * GP-FVM (arxiv 2406.05020, "PAPER.md") conditions a Gaussian-process prior
+ * on finite-volume observations of a linear PDE.  With a product Matérn
+ * kernel (Eq. 13) and factorized box schemes (§4
+ * Definition, l.306-313) the Gram matrix is a sum of Kronecker products of
+ * small 1D factor matrices (Eq. 20, l.316-318).  This library implements,
+ * on one sm_100a GPU in FP64:
+ *
+ *   gpfvm_assemble_factors   1D closed-form functional pairs (Eq. 10/16)
+ *   gpfvm_gram_matvec        Y = G X  for a block of vectors (Eq. 20)
+ *   gpfvm_solve              preconditioned CG / IterGP (§4.1, §4.2)
+ *   gpfvm_predict            posterior mean / variance on a grid (Eq. 5-6)
+ *
+ * Conventions (all entry points)
+ *   - Return value: GPFVM_OK (0) on success, a negative gpfvm_status
+ *     otherwise; gpfvm_last_error() returns a thread-local message.  Errors
+ *     never abort the process; a failing call leaves its outputs undefined.
+ *   - Memory: arrays inside *desc structs are HOST pointers, read during
+ *     the call and not retained.  Vector arguments (x, y, alpha, mean, var)
+ *     may be DEVICE pointers (fast path) or HOST pointers (pageable or
+ *     pinned): the library detects host memory with cudaPointerGetAttributes
+ *     and stages it through device buffers (host<->device copies are then
+ *     part of the call).  The caller owns all arrays it passes; the library
+ *     owns everything reachable from a gpfvm_problem handle.
+ *   - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).
+ *     Device-pointer calls are asynchronous w.r.t. the host unless stated;
+ *     host-pointer calls synchronise the stream before returning.
+ *   - Precision: every quantity is IEEE FP64.
+ *   - Layout of the observation vector: blocks in the order given; inside a
+ *     block, observations are the Cartesian product of the per-dimension
+ *     sites flattened row-major (dimension 0 slowest).  A block of vectors
+ *     is nrhs vectors of length N, vector r starting at x + r*ld (ld >= N).
+ *   - Thread safety: calls on distinct handles are independent; calls on one
+ *     handle must be serialised by the caller.
+ */
+#ifndef GPFVM_H
+#define GPFVM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPFVM_MAX_DIMS 4
+#define GPFVM_MAX_TERMS 16
+
+typedef enum {
+  GPFVM_OK = 0,
+  GPFVM_ERR_INVALID = -1,     /* bad argument / description */
+  GPFVM_ERR_CUDA = -2,        /* CUDA runtime error (message has details) */
+  GPFVM_ERR_UNSUPPORTED = -3, /* valid input outside what is implemented */
+  GPFVM_ERR_NUMERIC = -4,     /* breakdown (non-SPD, NaN) */
+  GPFVM_ERR_STATE = -5        /* call order violated (e.g. solve before assemble) */
+} gpfvm_status;
+
+/* Site kinds of a 1D functional list (PAPER.md l.170 point functionals;
+ * l.195-198 interval [a,b] functionals). */
+enum { GPFVM_SITE_POINT = 0, GPFVM_SITE_INTERVAL = 1 };
+
+/* One 1D Matérn factor, nu = q + 1/2 (Eq. 12, l.213-216):
+ *   k(d) = variance * exp(-sqrt(2q+1)|d|/l) * p_q(sqrt(2q+1)|d|/l),  0 <= q <= 3. */
+typedef struct {
+  int q;
+  double lengthscale;
+  double variance;
+} gpfvm_kernel1d;
+
+/* 1D site list: n sites of one kind.  For intervals lo[j] < hi[j]; for
+ * points lo[j] is the location (hi ignored).  Host pointers. */
+typedef struct {
+  int kind;
+  int n;
+  const double* lo;
+  const double* hi;
+} gpfvm_sites1d;
+
+/* One operator term  coeff * D^order [u_output]  (Eq. 18 preamble, l.267). */
+typedef struct {
+  double coeff;
+  int order[GPFVM_MAX_DIMS];
+  int output;
+} gpfvm_term;
+
+/* One factorized observation block (§4 Definition): per-dimension sites,
+ * the operator applied in every cell (Eq. 8/15), i.i.d. noise variance
+ * (Sigma, l.108) and whether the block is eliminated exactly in the
+ * preconditioner (IC/BC deflation, §4.2 l.331-339). */
+typedef struct {
+  gpfvm_sites1d sites[GPFVM_MAX_DIMS];
+  int n_terms;
+  gpfvm_term terms[GPFVM_MAX_TERMS];
+  double noise;
+  int deflate;
+} gpfvm_block;
+
+typedef struct {
+  int ndim;                          /* 1..GPFVM_MAX_DIMS */
+  int n_outputs;                     /* multi-output prior (Eq. 17) */
+  const gpfvm_kernel1d* kernels;     /* [n_outputs * ndim], output-major */
+  int n_blocks;
+  const gpfvm_block* blocks;
+} gpfvm_problem_desc;
+
+typedef struct gpfvm_problem gpfvm_problem;  /* opaque */
+
+/* ---- library / handle ------------------------------------------------- */
+const char* gpfvm_last_error(void);
+const char* gpfvm_version(void);
+
+/* Validate `desc`, copy it, allocate device storage on `device`.  Checks:
+ * ndim/q ranges, interval ordering, derivative orders (point order <= q,
+ * interval order <= q+1: PAPER.md §3.2 l.250 smoothness).  No GPU work. */
+int gpfvm_problem_create(const gpfvm_problem_desc* desc, int device, gpfvm_problem** out);
+int gpfvm_problem_destroy(gpfvm_problem* p);
+/* N (total number of observations). */
+int64_t gpfvm_problem_size(const gpfvm_problem* p);
+
+/* ---- §8 row 1: factor assembly ------------------------------------------
+ * Compute every 1D factor matrix  F[j,j'] = L_{left_j; m} k L'_{right_j'; m'}
+ * the Gram needs (Eq. 16, l.246; endpoint reduction Eq. 10, l.207) on the
+ * device, in double-double arithmetic from closed-form antiderivatives at
+ * the cell endpoints, rounded once to FP64.  Must precede
+ * matvec/solve/predict; may be called again (idempotent, bitwise
+ * reproducible). */
+int gpfvm_assemble_factors(gpfvm_problem* p, void* stream);
+
+/* Standalone single factor matrix into a caller DEVICE buffer `out`
+ * (row-major, left->n rows, right->n columns, leading dimension ld). */
+int gpfvm_factor_matrix(const gpfvm_kernel1d* k, const gpfvm_sites1d* left, int m_left,
+                        const gpfvm_sites1d* right, int m_right, double* out, int64_t ld,
+                        void* stream);
+
+/* ---- §8 row 2: Gram matvec ------------------------------------------------
+ * Y = G X + Sigma X for nrhs vectors (Eq. 20 + l.109), G never formed:
+ * batched mode-n contractions on FP64 tensor cores (DMMA).  x and y must not
+ * alias. */
+int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld,
+                      void* stream);
+
+/* ---- §8 row 3: solve -----------------------------------------------------
+ * Solve G alpha = y with preconditioned CG in IterGP form (§4.1; Wenger et
+ * al. 2022 Alg. 1, CG policy, full reorthogonalisation §6 l.475): actions
+ * s_i = P^{-1} r_{i-1}, G-conjugate directions d_i and eta_i = d_i^T G d_i
+ * are kept on the device for the computational-uncertainty downdate used by
+ * gpfvm_predict.  P is the block-LDL / fast-diagonalisation preconditioner
+ * built on the first call after assembly and cached.
+ * Stops when ||r||_2 <= rtol ||y||_2 (recursive residual) or after
+ * max_iter iterations; the report holds the final true residual too.
+ * nrhs must be 1 (multi-RHS systems: call once per column). */
+enum { GPFVM_PRECOND_NONE = 0, GPFVM_PRECOND_JACOBI = 1, GPFVM_PRECOND_BLOCK_FD = 2 };
+
+typedef struct {
+  double rtol;        /* default 1e-8 */
+  int max_iter;       /* default 1000 */
+  int precond;        /* GPFVM_PRECOND_* (default BLOCK_FD) */
+} gpfvm_solve_opts;
+
+typedef struct {
+  int iterations;
+  int converged;
+  double rel_residual;       /* recursive ||r_i|| / ||y|| */
+  double true_rel_residual;  /* ||y - G alpha|| / ||y||, recomputed */
+  double precond_shift;      /* Schur-complement shift used (0 normally) */
+  double setup_ms;           /* preconditioner build (first call) */
+  double iterate_ms;
+} gpfvm_solve_report;
+
+int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_solve_opts* opts,
+                gpfvm_solve_report* report, void* stream);
+
+/* ---- §8 row 4: predict -----------------------------------------------------
+ * Posterior on the tensor grid  X_* = pts[0] x ... x pts[ndim-1]  for
+ * output `output` (Eq. 5-6):
+ *   mean[g] = sum_J K_{*J} alpha_J        (cross-covariance Kronecker products)
+ *   var[g]  = k(x,x) - k_x^T C k_x        with C chosen by cov_mode:
+ *     GPFVM_COV_ITERGP  C = sum_i d_i d_i^T / eta_i  (IterGP combined posterior,
+ *                       the Krylov actions kept by the last gpfvm_solve)
+ *     GPFVM_COV_PRECOND C = P^{-1} (the exact posterior when
+ *                       P^{-1} = G^{-1}, e.g. the heat operator)
+ * mean/var: n_grid = prod n[i] entries, row-major (dim 0 slowest); either
+ * may be NULL to skip it.  alpha: the representer weights (length N). */
+enum { GPFVM_COV_ITERGP = 0, GPFVM_COV_PRECOND = 1 };
+
+typedef struct {
+  int n[GPFVM_MAX_DIMS];
+  const double* pts[GPFVM_MAX_DIMS];   /* host pointers */
+  int output;
+} gpfvm_grid;
+
+int gpfvm_predict(gpfvm_problem* p, const gpfvm_grid* grid, const double* alpha, double* mean,
+                  double* var, int cov_mode, void* stream);
+
+/* ---- instrumentation ------------------------------------------------------
+ * Kernel-launch counter (every kernel this library launches increments it)
+ * and per-kernel-class timing of the last matvec (CUDA events on `stream`). */
+int64_t gpfvm_launch_count(void);
+/* flops of one single-vector Gram matvec as executed (after the algebraic
+ * term cancellation of DESIGN.md R6), and of its dominant GEMM class. */
+double gpfvm_matvec_flops(const gpfvm_problem* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPFVM_H */

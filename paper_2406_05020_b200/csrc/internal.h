@@ -1,0 +1,129 @@
+// Internal declarations shared by the libgpfvm translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "../../include/gpfvm.h"
+#include "dd.cuh"
+
+namespace gpfvm {
+
+// ---- errors -----------------------------------------------------------------
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define GPFVM_CUDA(call)                                                                  \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::gpfvm::Error{GPFVM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e) + \
+                                               " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+  } while (0)
+
+#define GPFVM_CHECK(cond, code, msg)                  \
+  do {                                                \
+    if (!(cond)) throw ::gpfvm::Error{(code), (msg)}; \
+  } while (0)
+
+extern std::atomic<int64_t> g_launches;
+inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void check_launch(const char* what);
+
+// ---- device buffer -------------------------------------------------------------
+struct DevBuf {
+  double* ptr = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); ptr = o.ptr; n = o.n; o.ptr = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    release();
+    if (count == 0) return;
+    GPFVM_CUDA(cudaMalloc(&ptr, count * sizeof(double)));
+    n = count;
+  }
+};
+
+// ---- Matérn parameters in double-double ----------------------------------------
+struct MaternDD {
+  int q;
+  dd lam;
+  dd a[4];  // k(d) = exp(-lam d) * sum_k a[k] d^k  for d >= 0
+};
+MaternDD matern_dd(int q, double lengthscale, double variance);
+
+// site list resident on the device
+struct Sites {
+  int kind = GPFVM_SITE_INTERVAL;
+  int n = 0;
+  std::vector<double> lo, hi;
+  DevBuf d_lo, d_hi;
+};
+
+void launch_factor(const MaternDD& K, const Sites& L, int mL, const Sites& R, int mR, double* out,
+                   int64_t ld, cudaStream_t s);
+
+// ---- GEMM ------------------------------------------------------------------------
+// C[b] = alpha * A[b] * B[b] + beta * C[b] for b = (b1, b2), element strides.
+struct Gemm {
+  int M = 0, N = 0, K = 0;
+  int batch1 = 1, batch2 = 1;
+  const double* A = nullptr;
+  int64_t a_rs = 0, a_cs = 0, a_b1 = 0, a_b2 = 0;
+  const double* B = nullptr;
+  int64_t b_rs = 0, b_cs = 0, b_b1 = 0, b_b2 = 0;
+  double* C = nullptr;
+  int64_t c_rs = 0, c_cs = 0, c_b1 = 0, c_b2 = 0;
+  double alpha = 1.0, beta = 0.0;
+};
+void run_gemm(const Gemm& g, cudaStream_t s);
+double gemm_flops(const Gemm& g);
+
+// ---- small dense linear algebra (linalg.cu) ---------------------------------------
+// In-place lower Cholesky of an n x n row-major SPD matrix (upper part untouched).
+// Returns 0 on success, or the (1-based) failing column.
+int cholesky_inplace(double* A, int n, cudaStream_t s, int* d_info);
+// Solve L L^T X = B in place (B: n x nrhs, row-major, ld = nrhs) with L from cholesky_inplace.
+void cholesky_solve(const double* L, int n, double* B, int nrhs, cudaStream_t s);
+// X <- L^{-1} X  (forward substitution only)
+void trsm_lower(const double* L, int n, double* B, int nrhs, cudaStream_t s);
+// X <- U^{-1} X with U upper triangular (row-major, e.g. U = L^T)
+void trsm_upper(const double* U, int n, double* B, int nrhs, cudaStream_t s);
+// B (cols x rows) = A^T, A rows x cols, both row-major
+void transpose(const double* A, double* B, int rows, int cols, cudaStream_t s);
+// Generalised symmetric-definite eigenproblem  A V = Bm V diag(w),  V^T Bm V = I.
+// A, Bm: n x n row-major device; V: n x n row-major device (columns = eigenvectors); w: n.
+void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaStream_t s);
+
+// ---- vector ops (vecops.cu) --------------------------------------------------------
+void vec_scale_add(double* y, const double* x, const double* noise, int64_t n, int nrhs, int64_t ld,
+                   cudaStream_t s);  // y = noise .* x (per rhs)
+void dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, double* out,
+              cudaStream_t s);  // out[j] = X_j . v   (j < k)
+void axpy_many(double* y, const double* X, int64_t ldx, const double* coef, double sign, int64_t n,
+               int k, cudaStream_t s);  // y += sign * sum_j coef[j] X_j
+void fill(double* x, double v, int64_t n, cudaStream_t s);
+void copy(double* dst, const double* src, int64_t n, cudaStream_t s);
+void gather(double* dst, const double* src, const int64_t* idx, int64_t n, cudaStream_t s);
+void scatter(double* dst, const double* src, const int64_t* idx, int64_t n, cudaStream_t s);
+
+}  // namespace gpfvm

@@ -1,0 +1,287 @@
+// §8 row 4 — gpfvm_predict: posterior mean / variance on a tensor grid
+// (Eq. 5-6, l.113-114).
+//
+// The grid is a pseudo-block of point functionals of order 0 on output
+// `out`.  Its cross-covariance with block J is a sum of Kronecker products
+// of 1D cross factors  F(grid_i, 0; sites_J,i, alpha_i)  (Eq. 14, l.244),
+// assembled by the same double-double kernel as the Gram factors and applied
+// with the same DMMA mode products:
+//   mean = sum_J K_{*J} alpha_J
+//   var  = k(x,x) - k_x^T C k_x
+//     ITERGP : C = sum_i d_i d_i^T / eta_i        (rows of W = K_* D, downdate)
+//     PRECOND: C = P^{-1}, evaluated for the whole grid without a per-point
+//              solve: with (V(x)W)^T k_p = sum_tau c_tau (A_tau V)[t,:] (x) (B_tau W)[x,:]
+//              the FD part is  sum_{tau,tau'} c c' [(Â_tau o Â_tau') D^{-1} (B̂_tau o B̂_tau')^T]
+//              (three GEMMs per pair), and the IC/BC Schur part is
+//              z^T S^{-1} z with z = k_b - Y^T k_p, processed in grid slabs.
+#include <cmath>
+
+#include "problem.h"
+
+namespace gpfvm {
+
+
+namespace {
+
+__global__ void downdate_kernel(double* var, const double* __restrict__ W, const double* __restrict__ inv_eta,
+                                int k, int64_t ng, bool init, double prior) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    double v = init ? prior : var[g];
+    for (int j = 0; j < k; j++) {
+      double w = W[j * ng + g];
+      v -= w * w * inv_eta[j];
+    }
+    var[g] = v;
+  }
+}
+
+__global__ void hadamard_kernel(double* out, const double* __restrict__ a, const double* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a[i] * b[i];
+}
+
+// var[g] -= sum_c Z[c][g] T[c][g]
+__global__ void coldot_sub_kernel(double* var, const double* __restrict__ Z, const double* __restrict__ T, int nb,
+                                  int64_t ng) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nb; c++) s = fma(Z[(int64_t)c * ng + g], T[(int64_t)c * ng + g], s);
+    var[g] -= s;
+  }
+}
+
+__global__ void set_identity_kernel2(double* X, int n, int64_t ld) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int r = (int)(idx / n), c = (int)(idx % n);
+  X[r * ld + c] = (r == c) ? 1.0 : 0.0;
+}
+
+unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
+
+}  // namespace
+
+// cross factors between a grid (points, order 0) and every block with a term on `out`
+struct CrossPlan {
+  std::vector<Factor> factors;
+  std::vector<std::vector<KronTerm>> terms;  // per block J
+  int gshape[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
+  Sites gsites[GPFVM_MAX_DIMS];
+};
+
+static void build_cross(gpfvm_problem* p, const gpfvm_grid& g, int row0, int rows, CrossPlan& cp, cudaStream_t s) {
+  const int d = p->ndim;
+  for (int i = 0; i < d; i++) {
+    Sites& S = cp.gsites[i];
+    S.kind = GPFVM_SITE_POINT;
+    int off = (i == 0) ? row0 : 0;
+    S.n = (i == 0) ? rows : g.n[i];
+    S.lo.assign(g.pts[i] + off, g.pts[i] + off + S.n);
+    S.hi = S.lo;
+    S.d_lo.ensure(S.n);
+    S.d_hi.ensure(S.n);
+    GPFVM_CUDA(cudaMemcpyAsync(S.d_lo.ptr, S.lo.data(), S.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    GPFVM_CUDA(cudaMemcpyAsync(S.d_hi.ptr, S.lo.data(), S.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    cp.gshape[i] = S.n;
+  }
+  std::map<std::tuple<int, int, int>, int> idx;  // (dim, block, order) -> factor
+  cp.terms.assign(p->blocks.size(), {});
+  for (int J = 0; J < (int)p->blocks.size(); J++) {
+    const BlockInt& B = p->blocks[J];
+    for (const auto& t : B.terms) {
+      if (t.output != g.output) continue;
+      KronTerm kt;
+      kt.I = -1;
+      kt.J = J;
+      kt.coef = t.coeff;
+      for (int i = 0; i < d; i++) {
+        auto key = std::make_tuple(i, J, t.order[i]);
+        auto it = idx.find(key);
+        if (it == idx.end()) {
+          Factor F;
+          F.rows = cp.gsites[i].n;
+          F.cols = B.sites[i].n;
+          F.data.ensure((size_t)std::max(1, F.rows * F.cols));
+          const gpfvm_kernel1d& k = p->kernels[g.output * d + i];
+          launch_factor(matern_dd(k.q, k.lengthscale, k.variance), cp.gsites[i], 0, B.sites[i], t.order[i],
+                        F.data.ptr, F.cols, s);
+          cp.factors.push_back(std::move(F));
+          it = idx.emplace(key, (int)cp.factors.size() - 1).first;
+        }
+        kt.fid[i] = it->second;
+      }
+      cp.terms[J].push_back(kt);
+    }
+  }
+}
+
+// out[r] (grid slab) = sum_J K_{*J} X_J[r]  (overwrite), R vectors of stride ldx
+static void apply_cross(gpfvm_problem* p, CrossPlan& cp, const double* X, int64_t ldx, double* out, int64_t ldo, int R,
+                        double scale, bool overwrite, cudaStream_t s) {
+  bool first = overwrite;
+  for (int J = 0; J < (int)p->blocks.size(); J++) {
+    if (cp.terms[J].empty()) continue;
+    std::vector<KronTerm> ts = cp.terms[J];
+    for (auto& t : ts) t.coef *= scale;
+    std::vector<const KronTerm*> tp;
+    for (auto& t : ts) tp.push_back(&t);
+    apply_terms(p, cp.factors, tp, p->blocks[J].shape, cp.gshape, X + p->blocks[J].offset, ldx, out, ldo, R, first,
+                s, p->ws);
+    first = false;
+  }
+  if (first) {
+    int64_t ng = 1;
+    for (int i = 0; i < p->ndim; i++) ng *= cp.gshape[i];
+    for (int r = 0; r < R; r++) fill(out + r * ldo, 0.0, ng, s);
+  }
+}
+
+static double prior_var(gpfvm_problem* p, int out) {
+  double v = 1.0;
+  for (int i = 0; i < p->ndim; i++) v *= p->kernels[out * p->ndim + i].variance;
+  return v;
+}
+
+static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64_t ng, cudaStream_t s) {
+  GPFVM_CHECK(p->pc && p->pc->type == GPFVM_PRECOND_BLOCK_FD, GPFVM_ERR_STATE,
+              "GPFVM_COV_PRECOND needs a preceding gpfvm_solve with the BLOCK_FD preconditioner");
+  Precond& pc = *p->pc;
+  const int n0 = pc.n0, n1 = pc.n1;
+  const int g0 = cp.gshape[0], g1 = cp.gshape[1];
+  // --- FD part -------------------------------------------------------------
+  const auto& tP = cp.terms[pc.P];
+  std::vector<DevBuf> Ah(tP.size()), Bh(tP.size());
+  for (size_t a = 0; a < tP.size(); a++) {
+    const Factor& A = cp.factors[tP[a].fid[0]];  // g0 x n0
+    const Factor& B = cp.factors[tP[a].fid[1]];  // g1 x n1
+    Ah[a].ensure((size_t)g0 * n0);
+    Bh[a].ensure((size_t)g1 * n1);
+    Gemm g;
+    g.M = g0; g.N = n0; g.K = n0;
+    g.A = A.data.ptr; g.a_rs = n0; g.a_cs = 1;
+    g.B = pc.V.ptr; g.b_rs = n0; g.b_cs = 1;
+    g.C = Ah[a].ptr; g.c_rs = n0; g.c_cs = 1;
+    run_gemm(g, s);
+    g = Gemm();
+    g.M = g1; g.N = n1; g.K = n1;
+    g.A = B.data.ptr; g.a_rs = n1; g.a_cs = 1;
+    g.B = pc.W.ptr; g.b_rs = n1; g.b_cs = 1;
+    g.C = Bh[a].ptr; g.c_rs = n1; g.c_cs = 1;
+    run_gemm(g, s);
+  }
+  DevBuf Pm, Qm, M1;
+  Pm.ensure((size_t)g0 * n0);
+  Qm.ensure((size_t)g1 * n1);
+  M1.ensure((size_t)g0 * n1);
+  for (size_t a = 0; a < tP.size(); a++)
+    for (size_t b = a; b < tP.size(); b++) {
+      double w = tP[a].coef * tP[b].coef * (a == b ? 1.0 : 2.0);
+      hadamard_kernel<<<gs((int64_t)g0 * n0), 256, 0, s>>>(Pm.ptr, Ah[a].ptr, Ah[b].ptr, (int64_t)g0 * n0);
+      hadamard_kernel<<<gs((int64_t)g1 * n1), 256, 0, s>>>(Qm.ptr, Bh[a].ptr, Bh[b].ptr, (int64_t)g1 * n1);
+      count_launch(2);
+      Gemm g;
+      g.M = g0; g.N = n1; g.K = n0;
+      g.A = Pm.ptr; g.a_rs = n0; g.a_cs = 1;
+      g.B = pc.Dinv.ptr; g.b_rs = n1; g.b_cs = 1;
+      g.C = M1.ptr; g.c_rs = n1; g.c_cs = 1;
+      run_gemm(g, s);
+      g = Gemm();
+      g.M = g0; g.N = g1; g.K = n1;
+      g.A = M1.ptr; g.a_rs = n1; g.a_cs = 1;
+      g.B = Qm.ptr; g.b_rs = 1; g.b_cs = n1;
+      g.C = var; g.c_rs = g1; g.c_cs = 1;
+      g.alpha = -w; g.beta = 1.0;
+      run_gemm(g, s);
+    }
+  // --- IC/BC Schur part ----------------------------------------------------
+  if (pc.nb == 0) return;
+  const int nb = (int)pc.nb;
+  DevBuf Z, T, eye;
+  Z.ensure((size_t)nb * ng);
+  T.ensure((size_t)nb * ng);
+  // Z rows for deflated block J: K_{*J} e_l
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const int J = pc.bblocks[jb];
+    const int nJ = (int)p->blocks[J].size;
+    eye.ensure((size_t)nJ * nJ);
+    set_identity_kernel2<<<gs((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
+    count_launch();
+    std::vector<const KronTerm*> tp;
+    for (auto& t : cp.terms[J]) tp.push_back(&t);
+    if (tp.empty()) {
+      for (int r = 0; r < nJ; r++) fill(Z.ptr + (pc.boff[jb] + r) * ng, 0.0, ng, s);
+    } else {
+      apply_terms(p, cp.factors, tp, p->blocks[J].shape, cp.gshape, eye.ptr, nJ, Z.ptr + pc.boff[jb] * ng, ng, nJ,
+                  true, s, p->ws);
+    }
+  }
+  // Z -= K_{*P} Y  (rows of Y^T through the P cross terms, negated)
+  {
+    std::vector<KronTerm> ts = cp.terms[pc.P];
+    for (auto& t : ts) t.coef = -t.coef;
+    std::vector<const KronTerm*> tp;
+    for (auto& t : ts) tp.push_back(&t);
+    apply_terms(p, cp.factors, tp, p->blocks[pc.P].shape, cp.gshape, pc.YT.ptr, pc.Np, Z.ptr, ng, nb, false, s, p->ws);
+  }
+  // T = S^{-1} Z ; var -= colsum(Z o T)
+  Gemm g;
+  g.M = nb; g.N = (int)ng; g.K = nb;
+  g.A = pc.Sinv.ptr; g.a_rs = nb; g.a_cs = 1;
+  g.B = Z.ptr; g.b_rs = ng; g.b_cs = 1;
+  g.C = T.ptr; g.c_rs = ng; g.c_cs = 1;
+  run_gemm(g, s);
+  coldot_sub_kernel<<<gs(ng), 256, 0, s>>>(var, Z.ptr, T.ptr, nb, ng);
+  count_launch();
+}
+
+void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var, int cov_mode,
+                  cudaStream_t s) {
+  const int d = p->ndim;
+  int64_t ng = 1;
+  for (int i = 0; i < d; i++) ng *= g.n[i];
+  const double prior = prior_var(p, g.output);
+  if (mean) {
+    CrossPlan cp;
+    build_cross(p, g, 0, g.n[0], cp, s);
+    apply_cross(p, cp, alpha, p->N, mean, ng, 1, 1.0, true, s);
+  }
+  if (!var) return;
+  if (cov_mode == GPFVM_COV_ITERGP) {
+    CrossPlan cp;
+    build_cross(p, g, 0, g.n[0], cp, s);
+    Krylov& K = p->kry;
+    if (K.k == 0) {
+      fill(var, prior, ng, s);
+      return;
+    }
+    const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)(2e9 / 8 / std::max<int64_t>(ng, 1))));
+    DevBuf Wb, ie;
+    Wb.ensure((size_t)chunk * ng);
+    ie.ensure(K.k);
+    std::vector<double> inv(K.k);
+    for (int j = 0; j < K.k; j++) inv[j] = 1.0 / K.eta[j];
+    GPFVM_CUDA(cudaMemcpyAsync(ie.ptr, inv.data(), K.k * sizeof(double), cudaMemcpyHostToDevice, s));
+    for (int j0 = 0; j0 < K.k; j0 += chunk) {
+      int kc = std::min(chunk, K.k - j0);
+      apply_cross(p, cp, K.d.ptr + (int64_t)j0 * p->N, p->N, Wb.ptr, ng, kc, 1.0, true, s);
+      downdate_kernel<<<gs(ng), 256, 0, s>>>(var, Wb.ptr, ie.ptr + j0, kc, ng, j0 == 0, prior);
+      count_launch();
+    }
+    return;
+  }
+  // PRECOND: slabs along grid dim 0 to bound the nb x slab workspace
+  GPFVM_CHECK(d == 2, GPFVM_ERR_UNSUPPORTED, "GPFVM_COV_PRECOND: 2D problems only");
+  const int64_t per_row = g.n[1];
+  const int64_t nbv = p->pc ? std::max<int64_t>(1, p->pc->nb) : 1;
+  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(1.5e9 / 8 / (2 * nbv * per_row))));
+  for (int r0 = 0; r0 < g.n[0]; r0 += rows) {
+    int rr = std::min(rows, g.n[0] - r0);
+    CrossPlan cp;
+    build_cross(p, g, r0, rr, cp, s);
+    double* vslab = var + (int64_t)r0 * per_row;
+    fill(vslab, prior, (int64_t)rr * per_row, s);
+    var_precond_slab(p, cp, vslab, (int64_t)rr * per_row, s);
+  }
+}
+
+}  // namespace gpfvm

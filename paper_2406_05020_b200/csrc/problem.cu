@@ -1,0 +1,441 @@
+// C ABI: handle lifetime, factor assembly (§8 row 1) and the Kronecker Gram
+// matvec (§8 row 2).  See include/gpfvm.h for the contract and DESIGN.md §4.
+#include <cstring>
+#include <string>
+
+#include "problem.h"
+
+namespace gpfvm {
+
+static thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error{GPFVM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return GPFVM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GPFVM_ERR_INVALID;
+  }
+}
+
+static void upload_sites(Sites& s, cudaStream_t st) {
+  s.d_lo.ensure(std::max(1, s.n));
+  s.d_hi.ensure(std::max(1, s.n));
+  if (s.n > 0) {
+    GPFVM_CUDA(cudaMemcpyAsync(s.d_lo.ptr, s.lo.data(), s.n * sizeof(double), cudaMemcpyHostToDevice, st));
+    GPFVM_CUDA(cudaMemcpyAsync(s.d_hi.ptr, s.hi.data(), s.n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+}
+
+static void copy_sites(Sites& dst, const gpfvm_sites1d& src, int q_max_order_check) {
+  (void)q_max_order_check;
+  GPFVM_CHECK(src.kind == GPFVM_SITE_POINT || src.kind == GPFVM_SITE_INTERVAL, GPFVM_ERR_INVALID, "bad site kind");
+  GPFVM_CHECK(src.n >= 0, GPFVM_ERR_INVALID, "negative site count");
+  GPFVM_CHECK(src.n == 0 || src.lo != nullptr, GPFVM_ERR_INVALID, "sites.lo is NULL");
+  dst.kind = src.kind;
+  dst.n = src.n;
+  dst.lo.assign(src.lo, src.lo + src.n);
+  if (src.kind == GPFVM_SITE_INTERVAL) {
+    GPFVM_CHECK(src.n == 0 || src.hi != nullptr, GPFVM_ERR_INVALID, "sites.hi is NULL");
+    dst.hi.assign(src.hi, src.hi + src.n);
+    for (int j = 0; j < src.n; j++)
+      GPFVM_CHECK(dst.lo[j] < dst.hi[j], GPFVM_ERR_INVALID, "interval with lo >= hi");
+  } else {
+    dst.hi = dst.lo;
+  }
+}
+
+int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr) {
+  FactorKey key{out, dim, bl, ml, br, mr};
+  auto it = p->factor_index.find(key);
+  if (it != p->factor_index.end()) return it->second;
+  Factor f;
+  f.rows = p->blocks[bl].sites[dim].n;
+  f.cols = p->blocks[br].sites[dim].n;
+  p->factors.push_back(std::move(f));
+  int id = (int)p->factors.size() - 1;
+  p->factor_index[key] = id;
+  return id;
+}
+
+// Kronecker terms of all block pairs (Eq. 15/20 double sum), with the exact
+// algebraic cancellation of DESIGN.md R6 on diagonal blocks: for tau != tau'
+// the pair (tau', tau) equals prod_i s_i times the pair (tau, tau'),
+// s_i = (-1)^(alpha_i + alpha'_i), so the two merge into one term with
+// coefficient (1 + prod s_i) c c'.
+static void build_terms(gpfvm_problem* p) {
+  p->terms.clear();
+  const int nb = (int)p->blocks.size();
+  for (int I = 0; I < nb; I++)
+    for (int J = 0; J < nb; J++) {
+      const auto& TI = p->blocks[I].terms;
+      const auto& TJ = p->blocks[J].terms;
+      for (size_t a = 0; a < TI.size(); a++)
+        for (size_t b = 0; b < TJ.size(); b++) {
+          const gpfvm_term& t1 = TI[a];
+          const gpfvm_term& t2 = TJ[b];
+          if (t1.output != t2.output) continue;
+          double coef = t1.coeff * t2.coeff;
+          if (I == J && a != b) {
+            if (b < a) continue;
+            int par = 0;
+            for (int i = 0; i < p->ndim; i++) par += t1.order[i] + t2.order[i];
+            if (par & 1) continue;  // cancels against (b, a)
+            coef *= 2.0;
+          }
+          if (coef == 0.0) continue;
+          KronTerm kt;
+          kt.I = I;
+          kt.J = J;
+          kt.coef = coef;
+          for (int i = 0; i < p->ndim; i++) kt.fid[i] = get_factor(p, t1.output, i, I, t1.order[i], J, t2.order[i]);
+          p->terms.push_back(kt);
+        }
+    }
+}
+
+double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape) {
+  (void)p;
+  (void)t;
+  double fl = 0.0;
+  const int d = p->ndim;
+  for (int i = d - 1; i >= 0; i--) {
+    double outer = 1, inner = 1;
+    for (int k = 0; k < i; k++) outer *= in_shape[k];
+    for (int k = i + 1; k < d; k++) inner *= out_shape[k];
+    fl += 2.0 * outer * inner * in_shape[i] * (double)out_shape[i];
+  }
+  return fl;
+}
+
+void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std::vector<const KronTerm*>& terms, const int* in_shape,
+                 const int* out_shape, const double* x, int64_t ldx, double* y, int64_t ldy, int R,
+                 bool overwrite, cudaStream_t s, Workspace& ws) {
+  const int d = p->ndim;
+  // temp sizes: per vector, after stage i (dims i..d-1 converted)
+  int64_t maxsz = 0;
+  for (int i = d - 1; i >= 1; i--) {
+    int64_t sz = 1;
+    for (int k = 0; k < i; k++) sz *= in_shape[k];
+    for (int k = i; k < d; k++) sz *= out_shape[k];
+    maxsz = std::max(maxsz, sz);
+  }
+  if (d > 1) {
+    ws.t0.ensure((size_t)maxsz * R);
+    ws.t1.ensure((size_t)maxsz * R);
+  }
+  bool first_term = true;
+  for (const KronTerm* t : terms) {
+    const double* cur = x;
+    int64_t cur_ld = ldx;
+    for (int i = d - 1; i >= 0; i--) {
+      const Factor& F = factors[t->fid[i]];
+      int64_t outer = 1, inner = 1;
+      for (int k = 0; k < i; k++) outer *= in_shape[k];
+      for (int k = i + 1; k < d; k++) inner *= out_shape[k];
+      const int nin = in_shape[i], nout = out_shape[i];
+      double* dst;
+      int64_t dst_ld;
+      double alpha = 1.0, beta = 0.0;
+      if (i == 0) {
+        dst = y;
+        dst_ld = ldy;
+        alpha = t->coef;
+        beta = (overwrite && first_term) ? 0.0 : 1.0;
+      } else {
+        dst = ((d - 1 - i) % 2 == 0) ? ws.t0.ptr : ws.t1.ptr;
+        dst_ld = outer * nout * inner;
+      }
+      Gemm g;
+      g.alpha = alpha;
+      g.beta = beta;
+      if (inner == 1) {
+        // Y (outer x nout) = X (outer x nin) F^T
+        g.M = (int)outer; g.N = nout; g.K = nin;
+        g.A = cur; g.a_rs = nin; g.a_cs = 1; g.a_b1 = cur_ld;
+        g.B = F.data.ptr; g.b_rs = 1; g.b_cs = nin; g.b_b1 = 0;
+        g.C = dst; g.c_rs = nout; g.c_cs = 1; g.c_b1 = dst_ld;
+        g.batch1 = R; g.batch2 = 1;
+      } else {
+        // per (rhs, o): Y_o (nout x inner) = F (nout x nin) X_o (nin x inner)
+        g.M = nout; g.N = (int)inner; g.K = nin;
+        g.A = F.data.ptr; g.a_rs = nin; g.a_cs = 1; g.a_b1 = 0; g.a_b2 = 0;
+        g.B = cur; g.b_rs = inner; g.b_cs = 1; g.b_b1 = (int64_t)nin * inner; g.b_b2 = cur_ld;
+        g.C = dst; g.c_rs = inner; g.c_cs = 1; g.c_b1 = (int64_t)nout * inner; g.c_b2 = dst_ld;
+        g.batch1 = (int)outer; g.batch2 = R;
+      }
+      run_gemm(g, s);
+      cur = dst;
+      cur_ld = dst_ld;
+    }
+    first_term = false;
+  }
+  if (overwrite && first_term) {
+    // no terms: zero the output
+    int64_t osz = 1;
+    for (int k = 0; k < d; k++) osz *= out_shape[k];
+    for (int r = 0; r < R; r++) fill(y + r * ldy, 0.0, osz, s);
+  }
+}
+
+void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
+  GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_gram_matvec: call gpfvm_assemble_factors first");
+  vec_scale_add(y, x, p->noise.ptr, p->N, nrhs, ld, s);
+  const int nb = (int)p->blocks.size();
+  for (int I = 0; I < nb; I++)
+    for (int J = 0; J < nb; J++) {
+      std::vector<const KronTerm*> ts;
+      for (const auto& t : p->terms)
+        if (t.I == I && t.J == J) ts.push_back(&t);
+      if (ts.empty()) continue;
+      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[I].shape, x + p->blocks[J].offset, ld,
+                  y + p->blocks[I].offset, ld, nrhs, false, s, p->ws);
+    }
+}
+
+}  // namespace gpfvm
+
+using namespace gpfvm;
+
+gpfvm_problem::~gpfvm_problem() { destroy_precond(pc); }
+
+extern "C" {
+
+const char* gpfvm_last_error(void) { return g_err.c_str(); }
+const char* gpfvm_version(void) { return "gpfvm 0.1 (sm_100a, FP64 DMMA)"; }
+int64_t gpfvm_launch_count(void) { return g_launches.load(); }
+
+int gpfvm_problem_create(const gpfvm_problem_desc* desc, int device, gpfvm_problem** out) {
+  return guarded([&] {
+    GPFVM_CHECK(desc && out, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(desc->ndim >= 1 && desc->ndim <= GPFVM_MAX_DIMS, GPFVM_ERR_INVALID, "ndim out of range");
+    GPFVM_CHECK(desc->n_outputs >= 1, GPFVM_ERR_INVALID, "n_outputs < 1");
+    GPFVM_CHECK(desc->n_blocks >= 1 && desc->blocks, GPFVM_ERR_INVALID, "no blocks");
+    GPFVM_CHECK(desc->kernels != nullptr, GPFVM_ERR_INVALID, "kernels is NULL");
+    auto p = std::make_unique<gpfvm_problem>();
+    p->device = device;
+    p->ndim = desc->ndim;
+    p->nout = desc->n_outputs;
+    p->kernels.assign(desc->kernels, desc->kernels + desc->ndim * desc->n_outputs);
+    for (const auto& k : p->kernels) {
+      GPFVM_CHECK(k.q >= 0 && k.q <= 3, GPFVM_ERR_UNSUPPORTED, "Matérn q must be in [0,3]");
+      GPFVM_CHECK(k.lengthscale > 0 && k.variance > 0, GPFVM_ERR_INVALID, "lengthscale/variance must be > 0");
+    }
+    int64_t off = 0;
+    p->blocks.resize(desc->n_blocks);
+    for (int b = 0; b < desc->n_blocks; b++) {
+      const gpfvm_block& src = desc->blocks[b];
+      BlockInt& B = p->blocks[b];
+      GPFVM_CHECK(src.n_terms >= 1 && src.n_terms <= GPFVM_MAX_TERMS, GPFVM_ERR_INVALID, "block needs 1..16 terms");
+      GPFVM_CHECK(src.noise >= 0.0, GPFVM_ERR_INVALID, "negative noise");
+      B.size = 1;
+      for (int i = 0; i < desc->ndim; i++) {
+        copy_sites(B.sites[i], src.sites[i], 0);
+        B.shape[i] = B.sites[i].n;
+        B.size *= B.sites[i].n;
+      }
+      for (int t = 0; t < src.n_terms; t++) {
+        const gpfvm_term& tm = src.terms[t];
+        GPFVM_CHECK(tm.output >= 0 && tm.output < desc->n_outputs, GPFVM_ERR_INVALID, "term output out of range");
+        for (int i = 0; i < desc->ndim; i++) {
+          int q = p->kernels[tm.output * desc->ndim + i].q;
+          int m = tm.order[i];
+          GPFVM_CHECK(m >= 0, GPFVM_ERR_INVALID, "negative derivative order");
+          int o = (B.sites[i].kind == GPFVM_SITE_POINT) ? m : m - 1;
+          GPFVM_CHECK(o <= q, GPFVM_ERR_INVALID,
+                      "derivative order exceeds kernel smoothness (point order <= q, interval order <= q+1)");
+        }
+        B.terms.push_back(tm);
+      }
+      B.noise = src.noise;
+      B.deflate = src.deflate;
+      B.offset = off;
+      off += B.size;
+    }
+    p->N = off;
+    build_terms(p.get());
+    *out = p.release();
+  });
+}
+
+int gpfvm_problem_destroy(gpfvm_problem* p) {
+  return guarded([&] {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    delete p;
+  });
+}
+
+int64_t gpfvm_problem_size(const gpfvm_problem* p) { return p ? p->N : -1; }
+
+int gpfvm_assemble_factors(gpfvm_problem* p, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(p, GPFVM_ERR_INVALID, "null problem");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    for (auto& B : p->blocks)
+      for (int i = 0; i < p->ndim; i++) upload_sites(B.sites[i], s);
+    for (const auto& kv : p->factor_index) {
+      int out, dim, bl, ml, br, mr;
+      std::tie(out, dim, bl, ml, br, mr) = kv.first;
+      Factor& F = p->factors[kv.second];
+      F.data.ensure((size_t)std::max(1, F.rows * F.cols));
+      const gpfvm_kernel1d& k = p->kernels[out * p->ndim + dim];
+      MaternDD K = matern_dd(k.q, k.lengthscale, k.variance);
+      launch_factor(K, p->blocks[bl].sites[dim], ml, p->blocks[br].sites[dim], mr, F.data.ptr, F.cols, s);
+    }
+    p->noise.ensure(std::max<int64_t>(1, p->N));
+    for (const auto& B : p->blocks) fill(p->noise.ptr + B.offset, B.noise, B.size, s);
+    p->assembled = true;
+    destroy_precond(p->pc);  // factors changed: rebuild lazily
+    p->pc = nullptr;
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int gpfvm_factor_matrix(const gpfvm_kernel1d* k, const gpfvm_sites1d* left, int m_left, const gpfvm_sites1d* right,
+                        int m_right, double* out, int64_t ld, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(k && left && right && out, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(k->q >= 0 && k->q <= 3, GPFVM_ERR_UNSUPPORTED, "Matérn q must be in [0,3]");
+    GPFVM_CHECK(ld >= right->n, GPFVM_ERR_INVALID, "ld < right->n");
+    cudaStream_t s = (cudaStream_t)stream;
+    Sites L, R;
+    copy_sites(L, *left, 0);
+    copy_sites(R, *right, 0);
+    int oL = (L.kind == GPFVM_SITE_POINT) ? m_left : m_left - 1;
+    int oR = (R.kind == GPFVM_SITE_POINT) ? m_right : m_right - 1;
+    GPFVM_CHECK(m_left >= 0 && m_right >= 0 && oL <= k->q && oR <= k->q, GPFVM_ERR_INVALID,
+                "derivative order exceeds kernel smoothness");
+    upload_sites(L, s);
+    upload_sites(R, s);
+    launch_factor(matern_dd(k->q, k->lengthscale, k->variance), L, m_left, R, m_right, out, ld, s);
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(p && x && y, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(nrhs >= 1 && ld >= p->N, GPFVM_ERR_INVALID, "nrhs < 1 or ld < N");
+    GPFVM_CHECK(x != y, GPFVM_ERR_INVALID, "x and y must not alias");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool dx = is_device_ptr(x), dy = is_device_ptr(y);
+    const double* xd = x;
+    double* yd = y;
+    size_t n = (size_t)ld * (nrhs - 1) + p->N;
+    if (!dx) {
+      p->stage_in.ensure(n);
+      GPFVM_CUDA(cudaMemcpyAsync(p->stage_in.ptr, x, n * sizeof(double), cudaMemcpyHostToDevice, s));
+      xd = p->stage_in.ptr;
+    }
+    if (!dy) {
+      p->stage_out.ensure(n);
+      yd = p->stage_out.ptr;
+    }
+    matvec_device(p, xd, yd, nrhs, ld, s);
+    if (!dy) {
+      GPFVM_CUDA(cudaMemcpyAsync(y, yd, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      GPFVM_CUDA(cudaStreamSynchronize(s));
+    } else if (!dx) {
+      GPFVM_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+double gpfvm_matvec_flops(const gpfvm_problem* p) {
+  if (!p) return 0.0;
+  double fl = 0.0;
+  for (const auto& t : p->terms) fl += term_flops(p, t, p->blocks[t.J].shape, p->blocks[t.I].shape);
+  return fl;
+}
+
+int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_solve_opts* opts,
+                gpfvm_solve_report* report, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(p && y && alpha, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_solve: call gpfvm_assemble_factors first");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    gpfvm_solve_opts o{1e-8, 1000, GPFVM_PRECOND_BLOCK_FD};
+    if (opts) o = *opts;
+    GPFVM_CHECK(o.rtol >= 0 && o.max_iter >= 0, GPFVM_ERR_INVALID, "bad solve options");
+    gpfvm_solve_report rep{};
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool dy = is_device_ptr(y), da = is_device_ptr(alpha);
+    DevBuf ybuf, abuf;
+    const double* yd = y;
+    double* ad = alpha;
+    if (!dy) {
+      ybuf.ensure(p->N);
+      GPFVM_CUDA(cudaMemcpyAsync(ybuf.ptr, y, p->N * sizeof(double), cudaMemcpyHostToDevice, s));
+      yd = ybuf.ptr;
+    }
+    if (!da) {
+      abuf.ensure(p->N);
+      ad = abuf.ptr;
+    }
+    solve_impl(p, yd, ad, o, rep, s);
+    if (!da) GPFVM_CUDA(cudaMemcpyAsync(alpha, ad, p->N * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    if (report) *report = rep;
+  });
+}
+
+int gpfvm_predict(gpfvm_problem* p, const gpfvm_grid* grid, const double* alpha, double* mean, double* var,
+                  int cov_mode, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(p && grid && alpha, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_predict: call gpfvm_assemble_factors first");
+    GPFVM_CHECK(grid->output >= 0 && grid->output < p->nout, GPFVM_ERR_INVALID, "grid output out of range");
+    GPFVM_CHECK(cov_mode == GPFVM_COV_ITERGP || cov_mode == GPFVM_COV_PRECOND, GPFVM_ERR_INVALID, "bad cov_mode");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t ng = 1;
+    for (int i = 0; i < p->ndim; i++) {
+      GPFVM_CHECK(grid->n[i] >= 1 && grid->pts[i], GPFVM_ERR_INVALID, "empty grid dimension");
+      ng *= grid->n[i];
+    }
+    const bool da = is_device_ptr(alpha);
+    DevBuf abuf, mbuf, vbuf;
+    const double* ad = alpha;
+    if (!da) {
+      abuf.ensure(p->N);
+      GPFVM_CUDA(cudaMemcpyAsync(abuf.ptr, alpha, p->N * sizeof(double), cudaMemcpyHostToDevice, s));
+      ad = abuf.ptr;
+    }
+    double* md = mean;
+    double* vd = var;
+    if (mean && !is_device_ptr(mean)) { mbuf.ensure(ng); md = mbuf.ptr; }
+    if (var && !is_device_ptr(var)) { vbuf.ensure(ng); vd = vbuf.ptr; }
+    predict_impl(p, *grid, ad, md, vd, cov_mode, s);
+    if (mean && md != mean) GPFVM_CUDA(cudaMemcpyAsync(mean, md, ng * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (var && vd != var) GPFVM_CUDA(cudaMemcpyAsync(var, vd, ng * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+}  // extern "C"

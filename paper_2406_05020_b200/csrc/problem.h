@@ -1,0 +1,103 @@
+// The opaque gpfvm_problem handle and the Kronecker-term plan.
+#pragma once
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+namespace gpfvm {
+
+struct BlockInt {
+  Sites sites[GPFVM_MAX_DIMS];
+  std::vector<gpfvm_term> terms;
+  double noise = 0.0;
+  int deflate = 0;
+  int64_t size = 0, offset = 0;
+  int shape[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
+};
+
+// factor identity: (output, dim, left block, left order, right block, right order)
+using FactorKey = std::tuple<int, int, int, int, int, int>;
+
+struct Factor {
+  int rows = 0, cols = 0;
+  DevBuf data;  // row-major rows x cols
+};
+
+// coef * ((x)_i F_i) applied from block J (input) to block I (output)
+struct KronTerm {
+  int I = 0, J = 0;
+  double coef = 0.0;
+  int fid[GPFVM_MAX_DIMS] = {-1, -1, -1, -1};
+};
+
+// Block-LDL / fast-diagonalisation preconditioner state (solve.cu)
+struct Precond {
+  int type = GPFVM_PRECOND_NONE;
+  int P = -1;
+  int n0 = 0, n1 = 0;
+  int64_t Np = 0;
+  DevBuf V, Vt, W, Dinv;
+  std::vector<int> bblocks;
+  std::vector<int64_t> boff;  // offset of each deflated block inside the b-vector
+  int64_t nb = 0;
+  DevBuf GpbT, YT, Sinv;
+  double shift = 0.0;
+  DevBuf t1, t2, rb, zb, cvec;
+  double setup_ms = 0.0;
+};
+struct Krylov {   // kept IterGP actions
+  DevBuf d, gd;   // [cap][N]
+  std::vector<double> eta;
+  int k = 0, cap = 0;
+};
+
+struct Workspace {
+  DevBuf t0, t1;
+};
+
+}  // namespace gpfvm
+
+struct gpfvm_problem {
+  int device = 0;
+  int ndim = 0, nout = 0;
+  std::vector<gpfvm_kernel1d> kernels;  // [nout * ndim]
+  std::vector<gpfvm::BlockInt> blocks;
+  int64_t N = 0;
+  std::map<gpfvm::FactorKey, int> factor_index;
+  std::vector<gpfvm::Factor> factors;
+  std::vector<gpfvm::KronTerm> terms;
+  gpfvm::DevBuf noise;
+  bool assembled = false;
+  gpfvm::Workspace ws;
+  gpfvm::Precond* pc = nullptr;
+  gpfvm::Krylov kry;
+  gpfvm::DevBuf stage_in, stage_out;  // host-pointer staging
+  ~gpfvm_problem();
+};
+
+namespace gpfvm {
+
+// Apply the Kronecker terms of block pair (I, J) (or of the explicit term list)
+// to R vectors: Y_I (+)= sum coef (x)F X_J.  x/y strides per vector: ldx, ldy;
+// x and y point at the block starts.  beta_first = 0 overwrites Y on the first
+// term when `overwrite` is true.
+void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std::vector<const KronTerm*>& terms, const int* in_shape,
+                 const int* out_shape, const double* x, int64_t ldx, double* y, int64_t ldy, int R,
+                 bool overwrite, cudaStream_t s, Workspace& ws);
+void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s);
+double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape);
+int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr);
+
+bool is_device_ptr(const void* ptr);
+
+// solve.cu / predict.cu
+void solve_impl(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_solve_opts& o,
+                gpfvm_solve_report& rep, cudaStream_t s);
+void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var,
+                  int cov_mode, cudaStream_t s);
+void destroy_precond(Precond* pc);
+
+}  // namespace gpfvm

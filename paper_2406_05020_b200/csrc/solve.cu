@@ -1,0 +1,444 @@
+// §8 row 3 — gpfvm_solve: preconditioned CG in IterGP form.
+//
+// Preconditioner (built once per assembly, cached on the handle):
+//   FD for the single non-deflated 2D block P whose Gram keeps
+//       two Kronecker terms  c_a A0(x)A1 + c_b B0(x)B1  (exact for the heat
+//       operator, R6).  Generalised eigenproblems on the GPU (block Jacobi):
+//         B0 V = A0 V Lam (V^T A0 V = I),   A1 W = B1 W M (W^T B1 W = I)
+//       P^{-1}_PP = (V(x)W) D^{-1} (V(x)W)^T,  D_ij = c_a M_j + c_b Lam_i
+//       (+ block noise * |v_i|^2 |w_j|^2).
+//   block LDL (§5.2) over the deflated IC/BC blocks b (§4.2):
+//       Y = FD(G_pb), S = G_bb - G_pb^T Y (shifted only if Cholesky fails),
+//       P^{-1} r = [S^{-1}(r_b - G_pb^T FD r_p) ;  FD r_p - Y z_b].
+// Iteration (§4.1, Wenger et al. 2022 Alg. 1, CG policy, full
+// reorthogonalisation §6 l.475):
+//   s = P^{-1} r ; z = G s ; c_j = d_j.z / eta_j ; d = s - sum c_j d_j ;
+//   Gd = z - sum c_j Gd_j ; eta = z.d ; a = d.r / eta ; x += a d ; r -= a Gd
+#include <chrono>
+#include <cmath>
+
+#include "problem.h"
+
+namespace gpfvm {
+
+void destroy_precond(Precond* pc) { delete pc; }
+
+namespace {
+
+__global__ void scale_cols_kernel(double* X, const double* __restrict__ d, int64_t n, int R, int64_t ld) {
+  const int r = blockIdx.y;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    X[r * ld + i] *= d[i];
+}
+
+__global__ void colsumsq_kernel(const double* __restrict__ V, int n, double* out) {
+  // out[j] = sum_r V[r][j]^2  (V row-major n x n)
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < n; r++) s = fma(V[(int64_t)r * n + j], V[(int64_t)r * n + j], s);
+  out[j] = s;
+}
+
+__global__ void dinv_kernel(double* D, const double* __restrict__ lam, const double* __restrict__ mu,
+                            const double* __restrict__ vv, const double* __restrict__ ww, int n0, int n1,
+                            double ca, double cb, double noise) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n0 * n1) return;
+  int i = (int)(idx / n1), j = (int)(idx % n1);
+  double d = ca * mu[j] + cb * lam[i] + noise * vv[i] * ww[j];
+  D[idx] = 1.0 / d;
+}
+
+__global__ void set_identity_kernel(double* X, int n, int64_t ld) {
+  // X: n vectors of length n at stride ld
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int r = (int)(idx / n), c = (int)(idx % n);
+  X[r * ld + c] = (r == c) ? 1.0 : 0.0;
+}
+
+__global__ void add_diag_kernel(double* A, int n, const double* __restrict__ d, double shift) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) A[(int64_t)i * n + i] += (d ? d[i] : 0.0) + shift;
+}
+
+__global__ void sub_kernel(double* a, const double* __restrict__ b, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] -= b[i];
+}
+
+__global__ void symm_kernel(double* A, int n) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int r = (int)(idx / n), c = (int)(idx % n);
+  if (c <= r) return;
+  double v = 0.5 * (A[(int64_t)r * n + c] + A[(int64_t)c * n + r]);
+  A[(int64_t)r * n + c] = v;
+  A[(int64_t)c * n + r] = v;
+}
+
+unsigned g1(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// FD apply on R vectors (stride ldx in, ldy out), x != y
+static void fd_apply(Precond& pc, const double* x, int64_t ldx, double* y, int64_t ldy, int R, cudaStream_t s) {
+  const int n0 = pc.n0, n1 = pc.n1;
+  const int64_t np = pc.Np;
+  pc.t1.ensure((size_t)np * R);
+  pc.t2.ensure((size_t)np * R);
+  Gemm g;
+  // T1_r = X_r W
+  g = Gemm();
+  g.M = n0; g.N = n1; g.K = n1; g.batch1 = R;
+  g.A = x; g.a_rs = n1; g.a_cs = 1; g.a_b1 = ldx;
+  g.B = pc.W.ptr; g.b_rs = n1; g.b_cs = 1;
+  g.C = pc.t1.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
+  run_gemm(g, s);
+  // T2_r = V^T T1_r
+  g = Gemm();
+  g.M = n0; g.N = n1; g.K = n0; g.batch1 = R;
+  g.A = pc.Vt.ptr; g.a_rs = n0; g.a_cs = 1;
+  g.B = pc.t1.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = np;
+  g.C = pc.t2.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
+  run_gemm(g, s);
+  scale_cols_kernel<<<dim3(std::min<unsigned>(g1(np), 1184), R), 256, 0, s>>>(pc.t2.ptr, pc.Dinv.ptr, np, R, np);
+  count_launch();
+  // T1_r = V T2_r
+  g = Gemm();
+  g.M = n0; g.N = n1; g.K = n0; g.batch1 = R;
+  g.A = pc.V.ptr; g.a_rs = n0; g.a_cs = 1;
+  g.B = pc.t2.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = np;
+  g.C = pc.t1.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
+  run_gemm(g, s);
+  // Y_r = T1_r W^T
+  g = Gemm();
+  g.M = n0; g.N = n1; g.K = n1; g.batch1 = R;
+  g.A = pc.t1.ptr; g.a_rs = n1; g.a_cs = 1; g.a_b1 = np;
+  g.B = pc.W.ptr; g.b_rs = 1; g.b_cs = n1;
+  g.C = y; g.c_rs = n1; g.c_cs = 1; g.c_b1 = ldy;
+  run_gemm(g, s);
+}
+
+static const KronTerm* find_term(gpfvm_problem* p, int I, int J, int fid0, int fid1) {
+  for (const auto& t : p->terms)
+    if (t.I == I && t.J == J && t.fid[0] == fid0 && t.fid[1] == fid1) return &t;
+  return nullptr;
+}
+
+static void build_fd(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
+  const BlockInt& B = p->blocks[pc.P];
+  GPFVM_CHECK(p->ndim == 2 && B.terms.size() == 2, GPFVM_ERR_UNSUPPORTED,
+              "BLOCK_FD preconditioner needs a 2D non-deflated block with a two-term operator");
+  gpfvm_term ta = B.terms[0], tb = B.terms[1];
+  if (ta.order[0] < tb.order[0]) std::swap(ta, tb);
+  GPFVM_CHECK(ta.output == tb.output, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: terms on different outputs");
+  const int out = ta.output;
+  int fA0 = get_factor(p, out, 0, pc.P, ta.order[0], pc.P, ta.order[0]);
+  int fA1 = get_factor(p, out, 1, pc.P, ta.order[1], pc.P, ta.order[1]);
+  int fB0 = get_factor(p, out, 0, pc.P, tb.order[0], pc.P, tb.order[0]);
+  int fB1 = get_factor(p, out, 1, pc.P, tb.order[1], pc.P, tb.order[1]);
+  GPFVM_CHECK(find_term(p, pc.P, pc.P, fA0, fA1) && find_term(p, pc.P, pc.P, fB0, fB1), GPFVM_ERR_STATE,
+              "BLOCK_FD: diagonal term pairs missing");
+  pc.n0 = B.shape[0];
+  pc.n1 = B.shape[1];
+  pc.Np = B.size;
+  const int n0 = pc.n0, n1 = pc.n1;
+  DevBuf lam, mu, vv, ww;
+  lam.ensure(n0); mu.ensure(n1); vv.ensure(n0); ww.ensure(n1);
+  pc.V.ensure((size_t)n0 * n0);
+  pc.Vt.ensure((size_t)n0 * n0);
+  pc.W.ensure((size_t)n1 * n1);
+  pc.Dinv.ensure((size_t)n0 * n1);
+  sygv(p->factors[fB0].data.ptr, p->factors[fA0].data.ptr, n0, pc.V.ptr, lam.ptr, s);
+  sygv(p->factors[fA1].data.ptr, p->factors[fB1].data.ptr, n1, pc.W.ptr, mu.ptr, s);
+  transpose(pc.V.ptr, pc.Vt.ptr, n0, n0, s);
+  colsumsq_kernel<<<g1(n0, 128), 128, 0, s>>>(pc.V.ptr, n0, vv.ptr);
+  colsumsq_kernel<<<g1(n1, 128), 128, 0, s>>>(pc.W.ptr, n1, ww.ptr);
+  dinv_kernel<<<g1((int64_t)n0 * n1), 256, 0, s>>>(pc.Dinv.ptr, lam.ptr, mu.ptr, vv.ptr, ww.ptr, n0, n1,
+                                                   ta.coeff * ta.coeff, tb.coeff * tb.coeff, B.noise);
+  count_launch(3);
+  check_launch("build_fd");
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+}
+
+static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
+  const int nblk = (int)p->blocks.size();
+  pc.nb = 0;
+  for (int b = 0; b < nblk; b++)
+    if (p->blocks[b].deflate) {
+      pc.bblocks.push_back(b);
+      pc.boff.push_back(pc.nb);
+      pc.nb += p->blocks[b].size;
+    }
+  if (pc.nb == 0) return;
+  GPFVM_CHECK(pc.nb <= 16384, GPFVM_ERR_UNSUPPORTED, "block-LDL: more than 16384 deflated observations");
+  const int nb = (int)pc.nb;
+  const int64_t np = pc.Np;
+  pc.GpbT.ensure((size_t)nb * np);
+  pc.YT.ensure((size_t)nb * np);
+  DevBuf S, S0, eye, Lf;
+  S.ensure((size_t)nb * nb);
+  fill(S.ptr, 0.0, (int64_t)nb * nb, s);
+  // identity right-hand sides per deflated block, pushed through the Kronecker terms
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const int J = pc.bblocks[jb];
+    const int nJ = (int)p->blocks[J].size;
+    eye.ensure((size_t)nJ * nJ);
+    set_identity_kernel<<<g1((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
+    count_launch();
+    // rows of G_pb^T : (G_{P,J} e_c)^T
+    {
+      std::vector<const KronTerm*> ts;
+      for (const auto& t : p->terms)
+        if (t.I == pc.P && t.J == J) ts.push_back(&t);
+      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[pc.P].shape, eye.ptr, nJ,
+                  pc.GpbT.ptr + pc.boff[jb] * np, np, nJ, true, s, p->ws);
+    }
+    for (size_t ib = 0; ib < pc.bblocks.size(); ib++) {
+      const int I = pc.bblocks[ib];
+      std::vector<const KronTerm*> ts;
+      for (const auto& t : p->terms)
+        if (t.I == I && t.J == J) ts.push_back(&t);
+      if (ts.empty()) continue;
+      // vector c = G_{I,J} e_c -> S row (boff[J]+c), columns boff[I].. (S symmetric)
+      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[I].shape, eye.ptr, nJ,
+                  S.ptr + pc.boff[jb] * nb + pc.boff[ib], nb, nJ, true, s, p->ws);
+    }
+  }
+  // noise on the diagonal of G_bb
+  {
+    std::vector<double> nz(nb);
+    for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+      const BlockInt& B = p->blocks[pc.bblocks[jb]];
+      for (int64_t i = 0; i < B.size; i++) nz[pc.boff[jb] + i] = B.noise;
+    }
+    DevBuf dn;
+    dn.ensure(nb);
+    GPFVM_CUDA(cudaMemcpyAsync(dn.ptr, nz.data(), nb * sizeof(double), cudaMemcpyHostToDevice, s));
+    add_diag_kernel<<<g1(nb), 256, 0, s>>>(S.ptr, nb, dn.ptr, 0.0);
+    count_launch();
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  }
+  // Y^T = FD(G_pb) rows
+  fd_apply(pc, pc.GpbT.ptr, np, pc.YT.ptr, np, nb, s);
+  // S = G_bb - G_pb^T Y
+  {
+    Gemm g;
+    g.M = nb; g.N = nb; g.K = (int)np;
+    g.A = pc.GpbT.ptr; g.a_rs = np; g.a_cs = 1;
+    g.B = pc.YT.ptr; g.b_rs = 1; g.b_cs = np;
+    g.C = S.ptr; g.c_rs = nb; g.c_cs = 1;
+    g.alpha = -1.0; g.beta = 1.0;
+    run_gemm(g, s);
+  }
+  symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(S.ptr, nb);
+  count_launch();
+  // Cholesky with shift-on-failure
+  S0.ensure((size_t)nb * nb);
+  Lf.ensure((size_t)nb * nb);
+  copy(S0.ptr, S.ptr, (int64_t)nb * nb, s);
+  std::vector<double> diag(nb);
+  {
+    DevBuf dg;
+    dg.ensure(nb);
+    // fetch max diagonal (host) for the shift scale
+    std::vector<double> hS((size_t)nb * nb);
+    GPFVM_CUDA(cudaMemcpyAsync(hS.data(), S0.ptr, sizeof(double) * nb * nb, cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < nb; i++) diag[i] = hS[(size_t)i * nb + i];
+  }
+  double dmax = 0.0;
+  for (double v : diag) dmax = std::max(dmax, v);
+  int* d_info;
+  GPFVM_CUDA(cudaMalloc(&d_info, sizeof(int)));
+  double shift = 0.0;
+  for (int attempt = 0; attempt < 30; attempt++) {
+    copy(Lf.ptr, S0.ptr, (int64_t)nb * nb, s);
+    if (shift > 0.0) {
+      add_diag_kernel<<<g1(nb), 256, 0, s>>>(Lf.ptr, nb, nullptr, shift);
+      count_launch();
+    }
+    int info = cholesky_inplace(Lf.ptr, nb, s, d_info);
+    if (info == 0) break;
+    shift = (shift == 0.0) ? 1e-14 * dmax : shift * 10.0;
+    GPFVM_CHECK(attempt < 29, GPFVM_ERR_NUMERIC, "block-LDL: Schur complement not SPD even after shifting");
+  }
+  cudaFree(d_info);
+  pc.shift = shift;
+  // explicit S^{-1} (nb x nb) so each application is one multi-dot
+  pc.Sinv.ensure((size_t)nb * nb);
+  set_identity_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb, nb);
+  count_launch();
+  cholesky_solve(Lf.ptr, nb, pc.Sinv.ptr, nb, s);
+  symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb);
+  count_launch();
+  pc.rb.ensure(nb);
+  pc.zb.ensure(nb);
+  pc.cvec.ensure(nb);
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+}
+
+static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
+  if (p->pc && p->pc->type == type) return;
+  destroy_precond(p->pc);
+  p->pc = nullptr;
+  if (type == GPFVM_PRECOND_NONE) return;
+  GPFVM_CHECK(type == GPFVM_PRECOND_BLOCK_FD, GPFVM_ERR_UNSUPPORTED, "unsupported preconditioner");
+  double t0 = now_ms();
+  auto pc = new Precond();
+  try {
+    pc->type = type;
+    int ndefl = 0;
+    for (int b = 0; b < (int)p->blocks.size(); b++) {
+      if (!p->blocks[b].deflate) {
+        GPFVM_CHECK(pc->P < 0, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: exactly one non-deflated block supported");
+        pc->P = b;
+      } else {
+        ndefl++;
+      }
+    }
+    GPFVM_CHECK(pc->P >= 0, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: no non-deflated (PDE) block");
+    build_fd(p, *pc, s);
+    build_ldl(p, *pc, s);
+  } catch (...) {
+    delete pc;
+    throw;
+  }
+  pc->setup_ms = now_ms() - t0;
+  p->pc = pc;
+}
+
+// z = P^{-1} r (single vector, z != r)
+void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s) {
+  Precond& pc = *p->pc;
+  const BlockInt& BP = p->blocks[pc.P];
+  const double* rp = r + BP.offset;
+  double* zp = z + BP.offset;
+  fd_apply(pc, rp, pc.Np, zp, pc.Np, 1, s);
+  if (pc.nb == 0) return;
+  const int nb = (int)pc.nb;
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const BlockInt& B = p->blocks[pc.bblocks[jb]];
+    copy(pc.rb.ptr + pc.boff[jb], r + B.offset, B.size, s);
+  }
+  dot_many(pc.GpbT.ptr, pc.Np, zp, pc.Np, nb, pc.cvec.ptr, s);  // G_pb^T FD r_p
+  sub_kernel<<<g1(nb), 256, 0, s>>>(pc.rb.ptr, pc.cvec.ptr, nb);
+  count_launch();
+  dot_many(pc.Sinv.ptr, nb, pc.rb.ptr, nb, nb, pc.zb.ptr, s);    // z_b = S^{-1} t
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const BlockInt& B = p->blocks[pc.bblocks[jb]];
+    copy(z + B.offset, pc.zb.ptr + pc.boff[jb], B.size, s);
+  }
+  axpy_many(zp, pc.YT.ptr, pc.Np, pc.zb.ptr, -1.0, pc.Np, nb, s);  // z_p -= Y z_b
+}
+
+static void ensure_krylov(gpfvm_problem* p, int need, cudaStream_t s) {
+  Krylov& K = p->kry;
+  if (need <= K.cap) return;
+  int cap = std::max(need, std::max(8, K.cap * 2));
+  DevBuf d, gd;
+  d.ensure((size_t)cap * p->N);
+  gd.ensure((size_t)cap * p->N);
+  if (K.k > 0) {
+    copy(d.ptr, K.d.ptr, (int64_t)K.k * p->N, s);
+    copy(gd.ptr, K.gd.ptr, (int64_t)K.k * p->N, s);
+  }
+  K.d = std::move(d);
+  K.gd = std::move(gd);
+  K.cap = cap;
+}
+
+static double norm2(const double* v, int64_t n, double* dtmp, cudaStream_t s) {
+  dot_many(v, n, v, n, 1, dtmp, s);
+  double h;
+  GPFVM_CUDA(cudaMemcpyAsync(&h, dtmp, sizeof(double), cudaMemcpyDeviceToHost, s));
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+  return std::sqrt(h);
+}
+
+void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_opts& o, gpfvm_solve_report& rep,
+                cudaStream_t s) {
+  const int64_t N = p->N;
+  double t_setup0 = now_ms();
+  bool had = p->pc != nullptr && p->pc->type == o.precond;
+  build_precond(p, o.precond, s);
+  rep.setup_ms = had ? 0.0 : (now_ms() - t_setup0);
+  rep.precond_shift = p->pc ? p->pc->shift : 0.0;
+  double t0 = now_ms();
+  Krylov& K = p->kry;
+  K.k = 0;
+  K.eta.clear();
+  DevBuf r, sc;
+  r.ensure(N);
+  sc.ensure(std::max(8, o.max_iter + 8));
+  double* dsc = sc.ptr;  // scalars
+  copy(r.ptr, y, N, s);
+  fill(x, 0.0, N, s);
+  const double ny = norm2(y, N, dsc, s);
+  double nr = ny;
+  int it = 0;
+  rep.converged = 0;
+  if (ny == 0.0) {
+    rep.converged = 1;
+  }
+  std::vector<double> coef;
+  while (!rep.converged && it < o.max_iter) {
+    if (nr <= o.rtol * ny) {
+      rep.converged = 1;
+      break;
+    }
+    ensure_krylov(p, K.k + 1, s);
+    double* d = K.d.ptr + (int64_t)K.k * N;
+    double* gd = K.gd.ptr + (int64_t)K.k * N;
+    if (p->pc) precond_apply(p, r.ptr, d, s);
+    else copy(d, r.ptr, N, s);
+    matvec_device(p, d, gd, 1, N, s);  // z = G s (stored in gd)
+    if (K.k > 0) {
+      // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j
+      dot_many(K.d.ptr, N, gd, N, K.k, dsc, s);
+      coef.resize(K.k);
+      GPFVM_CUDA(cudaMemcpyAsync(coef.data(), dsc, sizeof(double) * K.k, cudaMemcpyDeviceToHost, s));
+      GPFVM_CUDA(cudaStreamSynchronize(s));
+      for (int j = 0; j < K.k; j++) coef[j] /= K.eta[j];
+      GPFVM_CUDA(cudaMemcpyAsync(dsc, coef.data(), sizeof(double) * K.k, cudaMemcpyHostToDevice, s));
+      axpy_many(d, K.d.ptr, N, dsc, -1.0, N, K.k, s);
+      axpy_many(gd, K.gd.ptr, N, dsc, -1.0, N, K.k, s);
+    }
+    // eta = Gd . d ; a = d . r / eta
+    dot_many(d, N, gd, N, 1, dsc, s);
+    dot_many(d, N, r.ptr, N, 1, dsc + 1, s);
+    double hs[2];
+    GPFVM_CUDA(cudaMemcpyAsync(hs, dsc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    const double eta = hs[0];
+    if (!(eta > 0.0) || !std::isfinite(eta)) break;  // breakdown: keep the trace so far
+    const double a = hs[1] / eta;
+    double ha[2] = {a, -a};
+    GPFVM_CUDA(cudaMemcpyAsync(dsc, ha, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+    axpy_many(x, d, N, dsc, 1.0, N, 1, s);
+    axpy_many(r.ptr, gd, N, dsc + 1, 1.0, N, 1, s);
+    K.eta.push_back(eta);
+    K.k++;
+    it++;
+    nr = norm2(r.ptr, N, dsc, s);
+  }
+  if (!rep.converged && nr <= o.rtol * ny) rep.converged = 1;
+  rep.iterations = it;
+  rep.rel_residual = ny > 0 ? nr / ny : 0.0;
+  rep.iterate_ms = now_ms() - t0;
+  // true residual
+  matvec_device(p, x, r.ptr, 1, N, s);
+  double one = 1.0;
+  GPFVM_CUDA(cudaMemcpyAsync(dsc, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  axpy_many(r.ptr, y, N, dsc, -1.0, N, 1, s);  // r = Gx - y
+  double tr = norm2(r.ptr, N, dsc + 1, s);
+  rep.true_rel_residual = ny > 0 ? tr / ny : 0.0;
+}
+
+}  // namespace gpfvm
