@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""GP-FVM hot-path benchmark (BASELINE.json metric: "FVM-Gram matvec GB/s & CG
+solve s to 1e-8 resid (N obs)").
+
+One step = one pass of every §8(a) row on BASELINE config 1 (1D heat,
+256 x 512 FVM cells + 1,024 IC/BC cells, Matérn-5/2, FP64):
+  1. gpfvm_assemble_factors
+  2. gpfvm_gram_matvec on a resident block of R = 128 vectors (135 MB > L2)
+  3. gpfvm_solve to relative residual 1e-8 (preconditioner built in-step)
+  4. gpfvm_predict mean + variance on the 512 x 1024 grid
+`value` = Gram-matvec throughput in GB/s: algorithmic bytes R*N*8*2 (read X,
+write Y) / matvec device time, summed over ranks / max over ranks.
+`cg_solve_s` = device time of row 3.  N > 1: independent replicas per rank
+(weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FVM-Gram matvec GB/s & CG solve s to 1e-8 resid (N obs)"
+WORKLOAD = "config1_heat1d_256x512"
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def cpu_baseline(seconds: float = 15.0):
+    """The oracle (as it stands) on the host cores: its plain Kronecker matvec
+    (oracle.gram.KroneckerGram) on config 1, vectors until ~`seconds` elapse."""
+    import numpy as np
+    import gpfvm_inputs as gi
+    from oracle.gram import KroneckerGram
+    p = gi.config1()
+    K = KroneckerGram(p)              # factor construction (mpmath) not timed
+    x = gi.random_vectors(p.size, 1, 3)[0]
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds or n == 0:
+        K.matvec(x)
+        n += 1
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    gbs = n * p.size * 8 * 2 / dt / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"{n} single-vector oracle Kronecker matvecs of config 1 (N={p.size}) in {dt:.1f}s; "
+                      f"factor construction excluded"}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return 0
+    steps_vals = []
+    per = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(seconds=per)
+        if i >= args.warmup:
+            steps_vals.append(cb)
+    val = sum(c["value"] for c in steps_vals) / len(steps_vals)
+    cb = dict(steps_vals[-1])
+    cb["value"] = val
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1000, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_obs": 132096, "note": "oracle Kronecker matvec on host cores"},
+            "cpu_baseline": cb, "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nrhs", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import gpfvm_inputs as gi
+    from paper_2406_05020_b200 import GpfvmProblem, launch_count
+    from paper_2406_05020_b200.build import build
+
+    rank, world, local = _dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+    dev = torch.device(f"cuda:{local}")
+
+    prob = gi.config1(seed=1 + rank)             # weak scaling: one replica per rank
+    grid = gi.heat_grid(512, 1024)
+    R = args.nrhs
+    gp = GpfvmProblem(prob, device=local)
+    N = gp.N
+    X = torch.tensor(gi.random_vectors(N, R, 11 + rank), dtype=torch.float64, device=dev)
+    Y = torch.empty_like(X)
+    rhs = torch.tensor(prob.rhs(), dtype=torch.float64, device=dev)
+    alpha = torch.empty_like(rhs)
+    mean = torch.empty(512 * 1024, dtype=torch.float64, device=dev)
+    var = torch.empty_like(mean)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step(timed: bool):
+        e = [ev() for _ in range(5)]
+        e[0].record()
+        gp.gpfvm_assemble_factors()
+        e[1].record()
+        gp.gpfvm_gram_matvec(X, out=Y)
+        e[2].record()
+        _, rep = gp.gpfvm_solve(rhs, rtol=1e-8, out=alpha)
+        e[3].record()
+        gp.gpfvm_predict(grid, alpha, cov_mode=1, mean=mean, var=var)
+        e[4].record()
+        return e, rep
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = launch_count()
+    times = {"assemble": [], "matvec": [], "solve": [], "predict": [], "step": []}
+    reps = []
+    with ClockSampler(local) as clk:
+        t_all0 = ev()
+        t_all1 = ev()
+        t_all0.record()
+        for _ in range(args.steps):
+            e, rep = step(True)
+            reps.append(rep)
+            torch.cuda.synchronize()
+            times["assemble"].append(e[0].elapsed_time(e[1]))
+            times["matvec"].append(e[1].elapsed_time(e[2]))
+            times["solve"].append(e[2].elapsed_time(e[3]))
+            times["predict"].append(e[3].elapsed_time(e[4]))
+            times["step"].append(e[0].elapsed_time(e[4]))
+        t_all1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = launch_count() - l0
+    total_ms = t_all0.elapsed_time(t_all1)
+    mv_ms = float(np.mean(times["matvec"]))
+    bytes_mv = R * N * 8 * 2
+    # max over ranks of the times, sum of the work
+    vals = torch.tensor([total_ms, mv_ms, float(np.mean(times["solve"]))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    total_ms, mv_ms_max, solve_ms_max = vals.tolist()
+    value = world * bytes_mv / (mv_ms_max * 1e-3) / 1e9
+
+    # e2e: same metric through the C ABI with pinned HOST buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((R, N), dtype=torch.float64, pin_memory=True)
+        Xh.copy_(X.cpu())
+        Yh = torch.empty((R, N), dtype=torch.float64, pin_memory=True)
+        xa, ya = Xh.numpy(), Yh.numpy()
+        gp.gpfvm_gram_matvec(xa, out=ya)
+        ts = []
+        for _ in range(max(2, args.steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            gp.gpfvm_gram_matvec(xa, out=ya)
+            ts.append(time.perf_counter() - t0)
+        e2e_s = float(np.median(ts))
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * bytes_mv / tt.item() / 1e9, "unit": "GB/s", "h2d_bytes_per_step": R * N * 8,
+               "d2h_bytes_per_step": R * N * 8}
+
+    flops_mv = gp.matvec_flops() * R
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    fp64_peak = 37.0  # TFLOP/s, DMMA.8x8x4 microbenchmark on this pool's B200 (profiles/fp64_peak.txt)
+    achieved = flops_mv / (mv_ms_max * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs)",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
+                "traffic": None, "flops_per_launch": flops_mv}
+
+    if rank == 0:
+        cb = None
+        if not args.no_cpu_baseline and world == 1:
+            cb = cpu_baseline(15.0)
+        rep = reps[-1]
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_obs": N, "n_pde": 256 * 512, "n_icbc": N - 256 * 512,
+                       "matvec_nrhs": R, "predict_grid": [512, 1024], "l2": "matvec block 135 MB > 126 MB L2",
+                       "parallelism": f"replicas{world}"},
+            "cg_solve_s": solve_ms_max / 1e3, "cg_iters": rep["iterations"],
+            "cg_true_rel_residual": rep["true_rel_residual"],
+            "ms": {k: float(np.mean(v)) for k, v in times.items()},
+            "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
+            "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

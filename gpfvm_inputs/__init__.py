@@ -204,6 +204,19 @@ def heat_grid(nt: int, nx: int) -> Grid:
     return Grid([np.linspace(0.0, 1.0, nt), np.linspace(0.0, 1.0, nx)], 0)
 
 
+def cos_ode_problem(n: int, q: int = 2, ell: float = 1.0) -> Problem:
+    """PAPER.md Fig. 2 (l.166): du/dx = cos(x) on [0, 2 pi], u(0) = u(2 pi) = 0,
+    n FVM cells; the cell observation int_a^b u' = u(b) - u(a) (Eq. 10) with
+    right-hand side int_a^b cos = sin(b) - sin(a)."""
+    X = cells(n, 0.0, 2 * np.pi)
+    rhs = np.sin(X.hi) - np.sin(X.lo)
+    blocks = [
+        Block("BC", [points([0.0, 2 * np.pi])], [Term(1.0, (0,))], 1e-10, True, np.zeros(2)),
+        Block("PDE", [X], [Term(1.0, (1,))], 0.0, False, rhs),
+    ]
+    return Problem(f"cos_ode_{n}", 1, [[Kernel1D(q, ell, 1.0)]], blocks, meta=dict(kind="cos_ode"))
+
+
 def random_vectors(n: int, nrhs: int, seed: int) -> np.ndarray:
     """Seeded standard-normal block of vectors, shape (nrhs, n)."""
     return np.random.default_rng(seed).standard_normal((nrhs, n))
