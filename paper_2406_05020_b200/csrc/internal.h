@@ -99,7 +99,7 @@ void run_gemm(const Gemm& g, cudaStream_t s);
 double gemm_flops(const Gemm& g);
 
 // ---- small dense linear algebra (linalg.cu) ---------------------------------------
-// In-place lower Cholesky of an n x n row-major SPD matrix (upper part untouched).
+// In-place lower Cholesky of an n x n row-major SPD matrix (strict upper part zeroed).
 // Returns 0 on success, or the (1-based) failing column.
 int cholesky_inplace(double* A, int n, cudaStream_t s, int* d_info);
 // Solve L L^T X = B in place (B: n x nrhs, row-major, ld = nrhs) with L from cholesky_inplace.

@@ -8,6 +8,9 @@
 //   * generalised symmetric-definite eigenproblem via Cholesky reduction.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -133,6 +136,12 @@ __global__ void symmetrize_kernel(double* A, int n) {
   A[(int64_t)c * n + r] = v;
 }
 
+__global__ void zero_upper_kernel(double* A, int n) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  if ((idx % n) > (idx / n)) A[idx] = 0.0;
+}
+
 __global__ void eye_kernel(double* A, int n) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -143,6 +152,7 @@ __global__ void eye_kernel(double* A, int n) {
 constexpr int JB = 16;          // columns per block
 constexpr int JC = 2 * JB;      // columns per CTA (pair of blocks)
 constexpr int JT = 512;         // threads per CTA
+__constant__ int c_inner_sweeps = 1;
 
 // Xc, Vc: column-major n x n (column j at Xc + j*n).  pairs: (blk_a, blk_b) per CTA.
 __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc, int n, int nblk,
@@ -175,16 +185,25 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
     Xs[(size_t)c * n + r] = Xc[(size_t)col_of[c] * n + r];
   }
   __syncthreads();
-  // Gram H = Xs^T Xs
-  for (int i = t; i < cnt * cnt; i += JT) {
-    int a = i / cnt, b = i % cnt;
-    if (b < a) continue;
-    const double* xa = Xs + (size_t)a * n;
-    const double* xb = Xs + (size_t)b * n;
-    double s = 0.0;
-    for (int r = 0; r < n; r++) s = fma(xa[r], xb[r], s);
-    H[a * (JC + 1) + b] = s;
-    H[b * (JC + 1) + a] = s;
+  // Gram H = Xs^T Xs: one warp per (a, b) entry, lanes stride the rows
+  // (consecutive lanes -> consecutive banks), shuffle reduction.
+  {
+    const int warp = t >> 5, lane = t & 31, nw = JT / 32;
+    const int npair = cnt * (cnt + 1) / 2;
+    for (int e = warp; e < npair; e += nw) {
+      int a = 0, rem = e;
+      while (rem >= cnt - a) { rem -= cnt - a; a++; }
+      int b = a + rem;
+      const double* xa = Xs + (size_t)a * n;
+      const double* xb = Xs + (size_t)b * n;
+      double s = 0.0;
+      for (int r = lane; r < n; r += 32) s = fma(xa[r], xb[r], s);
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) {
+        H[a * (JC + 1) + b] = s;
+        H[b * (JC + 1) + a] = s;
+      }
+    }
   }
   for (int i = t; i < JC * (JC + 1); i += JT) Q[i] = 0.0;
   __syncthreads();
@@ -205,7 +224,8 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
   __syncthreads();
   // parallel cyclic two-sided Jacobi on H (cnt x cnt), round-robin pairing
   const int m = (cnt + 1) & ~1;  // even player count (a dummy if cnt odd)
-  for (int sweep = 0; sweep < 12; sweep++) {
+  const int inner_sweeps = c_inner_sweeps;
+  for (int sweep = 0; sweep < inner_sweeps; sweep++) {
     __shared__ int done;
     if (t == 0) done = 1;
     __syncthreads();
@@ -288,7 +308,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
   }
 }
 
-__global__ void colnorm_kernel(const double* Xc, int n, double* w) {
+__global__ void colnorm_kernel(const double* Xc, int n, double* w, bool squared) {
   int j = blockIdx.x;
   double s = 0.0;
   for (int r = threadIdx.x; r < n; r += blockDim.x) s = fma(Xc[(size_t)j * n + r], Xc[(size_t)j * n + r], s);
@@ -299,7 +319,7 @@ __global__ void colnorm_kernel(const double* Xc, int n, double* w) {
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) w[j] = sqrt(red[0]);
+  if (threadIdx.x == 0) w[j] = squared ? red[0] : sqrt(red[0]);
 }
 
 }  // namespace
@@ -323,6 +343,8 @@ int cholesky_inplace(double* A, int n, cudaStream_t s, int* d_info) {
       run_gemm(g, s);
     }
   }
+  zero_upper_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(A, n);
+  count_launch();
   check_launch("cholesky");
   int info = 0;
   GPFVM_CUDA(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -383,13 +405,14 @@ void cholesky_solve(const double* L, int n, double* B, int nrhs, cudaStream_t s)
   GPFVM_CUDA(cudaStreamSynchronize(s));
 }
 
-// symmetric eigen-decomposition of SPD C (n x n row-major == column-major since symmetric).
-// V: row-major n x n with eigenvectors in columns; w: eigenvalues.
-static void syev_spd(const double* C, int n, double* V, double* w, cudaStream_t s) {
+// One-sided (Hestenes) block Jacobi on the columns of X (column-major n x n):
+// X W = U Sigma.  Eigenvectors of X^T X are the columns of W (returned row-major
+// in V, eigenvectors in columns); w = Sigma^2 (squared = true) or Sigma.
+static void jacobi_cols(const double* X0, int n, double* V, double* w, bool squared, cudaStream_t s) {
   DevBuf Xc, Vc;
   Xc.ensure((size_t)n * n);
   Vc.ensure((size_t)n * n);
-  GPFVM_CUDA(cudaMemcpyAsync(Xc.ptr, C, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  GPFVM_CUDA(cudaMemcpyAsync(Xc.ptr, X0, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
   eye_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(Vc.ptr, n);
   count_launch();
   int nblk = (n + JB - 1) / JB;
@@ -415,7 +438,11 @@ static void syev_spd(const double* C, int n, double* V, double* w, cudaStream_t 
   size_t smem = sizeof(double) * ((size_t)JC * n + 2 * JC * (JC + 1));
   GPFVM_CHECK(smem <= 227 * 1024, GPFVM_ERR_UNSUPPORTED, "eigensolver: dimension too large (n > 800)");
   GPFVM_CUDA(cudaFuncSetAttribute(jacobi_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sweeps = 0;
+  double offd = 1.0;
+  if (getenv("GPFVM_INNER")) { int v = atoi(getenv("GPFVM_INNER")); GPFVM_CUDA(cudaMemcpyToSymbol(c_inner_sweeps, &v, sizeof(int))); }
   for (int sweep = 0; sweep < 40; sweep++) {
+    sweeps++;
     GPFVM_CUDA(cudaMemsetAsync(d_off, 0, sizeof(unsigned long long), s));
     for (int r = 0; r < players - 1; r++) {
       jacobi_round_kernel<<<players / 2, JT, smem, s>>>(Xc.ptr, Vc.ptr, n, nblk, d_pairs + r * players, d_off);
@@ -425,11 +452,13 @@ static void syev_spd(const double* C, int n, double* V, double* w, cudaStream_t 
     unsigned long long off = 0;
     GPFVM_CUDA(cudaMemcpyAsync(&off, d_off, sizeof(off), cudaMemcpyDeviceToHost, s));
     GPFVM_CUDA(cudaStreamSynchronize(s));
-    double offd;
     memcpy(&offd, &off, sizeof(double));
-    if (offd < 1e-15) break;
+    if (getenv("GPFVM_DEBUG") && atoi(getenv("GPFVM_DEBUG")) > 1) fprintf(stderr, "[gpfvm]   sweep %d off %.3e\n", sweep, offd);
+    // one-sided Jacobi orthogonality floor ~ n eps (rounding of the column dots)
+    if (offd < std::max(4e-15, 2e-16 * n)) break;
   }
-  colnorm_kernel<<<n, 256, 0, s>>>(Xc.ptr, n, w);
+  if (getenv("GPFVM_DEBUG")) fprintf(stderr, "[gpfvm] jacobi n=%d sweeps=%d offmax=%.3e\n", n, sweeps, offd);
+  colnorm_kernel<<<n, 256, 0, s>>>(Xc.ptr, n, w, squared);
   count_launch();
   // Vc is column-major; V row-major with eigenvectors in columns == transpose of Vc storage
   transpose(Vc.ptr, V, n, n, s);
@@ -439,6 +468,10 @@ static void syev_spd(const double* C, int n, double* V, double* w, cudaStream_t 
 }
 
 void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaStream_t s) {
+  // A V = Bm V diag(w), V^T Bm V = I.  With Bm = L L^T and (if A is SPD) A = M M^T,
+  // C = L^{-1} A L^{-T} = G G^T for G = L^{-1} M, so one-sided Jacobi on the
+  // columns of G^T (condition sqrt(kappa(C))) gives C's eigenvectors W and
+  // w = sigma^2; V = L^{-T} W.  If A is not SPD, C itself is used (w = sigma).
   DevBuf L, W, Wt, U;
   L.ensure((size_t)n * n);
   W.ensure((size_t)n * n);
@@ -448,15 +481,22 @@ void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaSt
   GPFVM_CUDA(cudaMalloc(&d_info, sizeof(int)));
   GPFVM_CUDA(cudaMemcpyAsync(L.ptr, Bm, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
   int info = cholesky_inplace(L.ptr, n, s, d_info);
-  cudaFree(d_info);
   GPFVM_CHECK(info == 0, GPFVM_ERR_NUMERIC, "sygv: B factor not positive definite (column " + std::to_string(info) + ")");
   GPFVM_CUDA(cudaMemcpyAsync(W.ptr, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
-  trsm_lower(L.ptr, n, W.ptr, n, s);          // W = L^{-1} A
-  transpose(W.ptr, Wt.ptr, n, n, s);          // Wt = A L^{-T}
-  trsm_lower(L.ptr, n, Wt.ptr, n, s);         // C = L^{-1} A L^{-T}
-  symmetrize_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(Wt.ptr, n);
-  count_launch();
-  syev_spd(Wt.ptr, n, U.ptr, w, s);           // C = U diag(w) U^T
+  int infoA = cholesky_inplace(W.ptr, n, s, d_info);
+  cudaFree(d_info);
+  if (infoA == 0) {
+    trsm_lower(L.ptr, n, W.ptr, n, s);        // G = L^{-1} M (row-major) == column-major G^T
+    jacobi_cols(W.ptr, n, U.ptr, w, true, s);
+  } else {
+    GPFVM_CUDA(cudaMemcpyAsync(W.ptr, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+    trsm_lower(L.ptr, n, W.ptr, n, s);        // W = L^{-1} A
+    transpose(W.ptr, Wt.ptr, n, n, s);        // Wt = A L^{-T}
+    trsm_lower(L.ptr, n, Wt.ptr, n, s);       // C = L^{-1} A L^{-T}
+    symmetrize_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(Wt.ptr, n);
+    count_launch();
+    jacobi_cols(Wt.ptr, n, U.ptr, w, false, s);
+  }
   transpose(L.ptr, W.ptr, n, n, s);           // W = L^T (upper)
   trsm_upper(W.ptr, n, U.ptr, n, s);          // V = L^{-T} U
   GPFVM_CUDA(cudaMemcpyAsync(V, U.ptr, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
