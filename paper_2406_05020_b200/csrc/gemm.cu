@@ -1,14 +1,22 @@
 // FP64 tensor-core GEMM (DMMA m8n8k4) for the batched mode-n contractions of
 // the Kronecker matvec.
 //
-// C[b] = alpha * A[b] B[b] + beta * C[b],  b = (b1, b2) two-level batch.
+//   C[b] = alpha * sum_seg A_seg[b] B_seg[b] + beta * C[b]
+//   b = (b1, b2, b3) three-level batch, seg = 0..nseg-1 K-segments
+//   (A_seg = A + seg*a_sg, B_seg = B + seg*b_sg): a sum of Kronecker terms
+//   whose contraction inputs live side by side becomes ONE GEMM with
+//   K_total = nseg*K (DESIGN.md §4.2 "K-concatenation").
 // Fast path: A row-major (a_cs == 1), C row-major (c_cs == 1), B row-major
 // (b_cs == 1) or column-major (b_rs == 1).  Tiles are staged through shared
-// memory with a 3-stage cp.async pipeline; each warp owns a (TM*8)x(TN*8)
-// sub-tile and issues TM*TN DMMA per k4 step (SASS: DMMA.8x8x4, the only
-// FP64 tensor-core instruction on sm_100a — tcgen05 has no f64 kind).
-// Shared-memory rows are padded so the fragment loads hit each 8-byte bank
-// pair exactly twice per warp (2 wavefronts, the minimum for 256 B).
+// memory by a multi-stage cp.async pipeline (16-byte copies when every
+// address is 16-byte aligned, else 8-byte), each warp owns a (TM*8)x(TN*8)
+// sub-tile and issues TM*TN DMMA per k4 step (SASS DMMA.8x8x4 — the FP64
+// tensor-core instruction of sm_100a; tcgen05 has no f64 kind).  Shared rows
+// are padded so fragment loads hit each 8-byte bank pair exactly twice per
+// warp (2 wavefronts, the minimum for 256 B).
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace gpfvm {
@@ -16,14 +24,18 @@ namespace gpfvm {
 namespace {
 
 constexpr int BK = 16;
-constexpr int STAGES = 3;
-constexpr int APAD = 4;   // As row stride BK+4 doubles
-constexpr int BPAD = 8;   // Bs (row layout) row stride BN+8 doubles
+constexpr int APAD = 4;   // As row stride BK+4 doubles (160 B, 16-B aligned)
+constexpr int BPAD = 4;   // Bs (row layout) row stride BN+4 doubles: (k*stride) mod 16 in {0,4,8,12} per half-warp
 
 __device__ __forceinline__ void cp_async8(void* smem, const double* gmem, bool pred) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int sz = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const double* gmem, int valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid * 8;  // 0, 8 or 16 bytes, rest zero-filled
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -37,29 +49,40 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_ROW>
+template <int BM, int BN, bool B_ROW>
+struct SmemLayout {
+  static constexpr int AS = BK + APAD;
+  static constexpr int BS_ROW = BN + BPAD;
+  static constexpr int A_STAGE = BM * AS;
+  static constexpr int B_STAGE = B_ROW ? BK * BS_ROW : BN * AS;
+};
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool B_ROW, bool V16>
 __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     dgemm_dmma_kernel(Gemm g) {
   constexpr int NT = WARPS_M * WARPS_N * 32;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
   constexpr int TM = WM / 8, TN = WN / 8;
-  constexpr int AS = BK + APAD;
-  constexpr int BS_ROW = BN + BPAD;
-  constexpr int B_STAGE = B_ROW ? BK * BS_ROW : BN * AS;
+  using L = SmemLayout<BM, BN, B_ROW>;
+  constexpr int AS = L::AS, BS_ROW = L::BS_ROW;
   extern __shared__ __align__(16) double smem[];
-  double* As = smem;                       // [STAGES][BM][AS]
-  double* Bs = smem + STAGES * BM * AS;    // [STAGES][BK][BS_ROW] or [STAGES][BN][AS]
+  double* As = smem;
+  double* Bs = smem + STAGES * L::A_STAGE;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  const int KT = (g.K + BK - 1) / BK;
+  const int KT_all = KT * g.nseg;
 
-  for (int64_t z = blockIdx.z; z < (int64_t)g.batch1 * g.batch2; z += gridDim.z) {
-    const int64_t b1 = z % g.batch1, b2 = z / g.batch1;
-    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
-    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2;
-    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2;
+  for (int64_t z = blockIdx.z; z < nbatch; z += gridDim.z) {
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3;
+    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3;
 
     double acc[TM][TN][2];
 #pragma unroll
@@ -67,55 +90,84 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
 #pragma unroll
       for (int j = 0; j < TN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int KT = (g.K + BK - 1) / BK;
-    auto load_tile = [&](int stage, int kt) {
-      const int k0 = kt * BK;
-      double* as = As + stage * BM * AS;
+    auto load_tile = [&](int stage, int kt_all) {
+      const int seg = kt_all / KT;
+      const int k0 = (kt_all - seg * KT) * BK;
+      const double* Aseg = A + seg * g.a_sg;
+      const double* Bseg = B + seg * g.b_sg;
+      double* as = As + stage * L::A_STAGE;
+      double* bs = Bs + stage * L::B_STAGE;
+      if (V16) {
 #pragma unroll
-      for (int i = tid; i < BM * BK; i += NT) {
-        int r = i / BK, c = i % BK;
-        int gm = m0 + r, gk = k0 + c;
-        bool p = (gm < g.M) && (gk < g.K);
-        const double* src = p ? (A + (int64_t)gm * g.a_rs + gk) : A;
-        cp_async8(as + r * AS + c, src, p);
-      }
-      double* bs = Bs + stage * B_STAGE;
-      if (B_ROW) {
+        for (int i = tid; i < BM * BK / 2; i += NT) {
+          int r = i / (BK / 2), c = (i % (BK / 2)) * 2;
+          int gm = m0 + r, gk = k0 + c;
+          int valid = (gm < g.M) ? max(0, min(2, g.K - gk)) : 0;
+          const double* src = valid ? (Aseg + (int64_t)gm * g.a_rs + gk) : Aseg;
+          cp_async16(as + r * AS + c, src, valid);
+        }
+        if (B_ROW) {
 #pragma unroll
-        for (int i = tid; i < BK * BN; i += NT) {
-          int r = i / BN, c = i % BN;
-          int gk = k0 + r, gn = n0 + c;
-          bool p = (gk < g.K) && (gn < g.N);
-          const double* src = p ? (B + (int64_t)gk * g.b_rs + gn) : B;
-          cp_async8(bs + r * BS_ROW + c, src, p);
+          for (int i = tid; i < BK * BN / 2; i += NT) {
+            int r = i / (BN / 2), c = (i % (BN / 2)) * 2;
+            int gk = k0 + r, gn = n0 + c;
+            int valid = (gk < g.K) ? max(0, min(2, g.N - gn)) : 0;
+            const double* src = valid ? (Bseg + (int64_t)gk * g.b_rs + gn) : Bseg;
+            cp_async16(bs + r * BS_ROW + c, src, valid);
+          }
+        } else {
+#pragma unroll
+          for (int i = tid; i < BN * BK / 2; i += NT) {
+            int r = i / (BK / 2), c = (i % (BK / 2)) * 2;  // r: n, c: k
+            int gn = n0 + r, gk = k0 + c;
+            int valid = (gn < g.N) ? max(0, min(2, g.K - gk)) : 0;
+            const double* src = valid ? (Bseg + (int64_t)gn * g.b_cs + gk) : Bseg;
+            cp_async16(bs + r * AS + c, src, valid);
+          }
         }
       } else {
 #pragma unroll
-        for (int i = tid; i < BK * BN; i += NT) {
-          int r = i / BK, c = i % BK;  // r: n, c: k
-          int gn = n0 + r, gk = k0 + c;
-          bool p = (gk < g.K) && (gn < g.N);
-          const double* src = p ? (B + (int64_t)gn * g.b_cs + gk) : B;
-          cp_async8(bs + r * AS + c, src, p);
+        for (int i = tid; i < BM * BK; i += NT) {
+          int r = i / BK, c = i % BK;
+          int gm = m0 + r, gk = k0 + c;
+          bool p = (gm < g.M) && (gk < g.K);
+          cp_async8(as + r * AS + c, p ? (Aseg + (int64_t)gm * g.a_rs + gk) : Aseg, p);
+        }
+        if (B_ROW) {
+#pragma unroll
+          for (int i = tid; i < BK * BN; i += NT) {
+            int r = i / BN, c = i % BN;
+            int gk = k0 + r, gn = n0 + c;
+            bool p = (gk < g.K) && (gn < g.N);
+            cp_async8(bs + r * BS_ROW + c, p ? (Bseg + (int64_t)gk * g.b_rs + gn) : Bseg, p);
+          }
+        } else {
+#pragma unroll
+          for (int i = tid; i < BK * BN; i += NT) {
+            int r = i / BK, c = i % BK;
+            int gn = n0 + r, gk = k0 + c;
+            bool p = (gk < g.K) && (gn < g.N);
+            cp_async8(bs + r * AS + c, p ? (Bseg + (int64_t)gn * g.b_cs + gk) : Bseg, p);
+          }
         }
       }
     };
 
 #pragma unroll
     for (int s = 0; s < STAGES - 1; s++) {
-      if (s < KT) load_tile(s, s);
+      if (s < KT_all) load_tile(s, s);
       cp_async_commit();
     }
-    for (int kt = 0; kt < KT; kt++) {
+    for (int kt = 0; kt < KT_all; kt++) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       {
         int nk = kt + STAGES - 1;
-        if (nk < KT) load_tile(nk % STAGES, nk);
+        if (nk < KT_all) load_tile(nk % STAGES, nk);
         cp_async_commit();
       }
-      const double* as = As + (kt % STAGES) * BM * AS;
-      const double* bs = Bs + (kt % STAGES) * B_STAGE;
+      const double* as = As + (kt % STAGES) * L::A_STAGE;
+      const double* bs = Bs + (kt % STAGES) * L::B_STAGE;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         double af[TM], bf[TN];
@@ -137,7 +189,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
     cp_async_wait<0>();
     __syncthreads();
 
-    // epilogue: C = alpha acc + beta C
+    // epilogue: C = alpha acc + beta C  (2 consecutive doubles per thread)
 #pragma unroll
     for (int i = 0; i < TM; i++) {
       int row = m0 + wm0 + i * 8 + (lane >> 2);
@@ -159,19 +211,25 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
   }
 }
 
-// Generic strided fallback (small / irregular shapes): one thread per C entry.
+// Generic strided fallback (tiny / irregular shapes): one thread per C entry.
 __global__ void dgemm_generic_kernel(Gemm g) {
-  int64_t total = (int64_t)g.M * g.N;
-  for (int64_t z = blockIdx.y; z < (int64_t)g.batch1 * g.batch2; z += gridDim.y) {
-    const int64_t b1 = z % g.batch1, b2 = z / g.batch1;
-    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
-    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2;
-    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2;
+  const int64_t total = (int64_t)g.M * g.N;
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  for (int64_t z = blockIdx.y; z < nbatch; z += gridDim.y) {
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3;
+    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
       int m = (int)(idx / g.N), n = (int)(idx % g.N);
       double acc = 0.0;
-      for (int k = 0; k < g.K; k++) acc = fma(A[m * g.a_rs + k * g.a_cs], B[k * g.b_rs + n * g.b_cs], acc);
+      for (int seg = 0; seg < g.nseg; seg++) {
+        const double* As = A + seg * g.a_sg;
+        const double* Bs = B + seg * g.b_sg;
+        for (int k = 0; k < g.K; k++) acc = fma(As[m * g.a_rs + k * g.a_cs], Bs[k * g.b_rs + n * g.b_cs], acc);
+      }
       double* cp = C + m * g.c_rs + n * g.c_cs;
       double v = g.alpha * acc;
       if (g.beta != 0.0) v += g.beta * *cp;
@@ -180,59 +238,77 @@ __global__ void dgemm_generic_kernel(Gemm g) {
   }
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N, bool B_ROW>
+template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool B_ROW, bool V16>
 void launch_dmma(const Gemm& g, cudaStream_t s) {
-  constexpr int AS = BK + APAD;
-  constexpr int B_STAGE = B_ROW ? BK * (BN + BPAD) : BN * AS;
-  size_t smem = (size_t)STAGES * (BM * AS + B_STAGE) * sizeof(double);
-  auto kern = dgemm_dmma_kernel<BM, BN, WARPS_M, WARPS_N, B_ROW>;
-  static bool configured = false;
-  if (!configured) {
+  using L = SmemLayout<BM, BN, B_ROW>;
+  size_t smem = (size_t)STAGES * (L::A_STAGE + L::B_STAGE) * sizeof(double);
+  auto kern = dgemm_dmma_kernel<BM, BN, WARPS_M, WARPS_N, STAGES, B_ROW, V16>;
+  static int configured_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured_dev != dev) {
     GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+    configured_dev = dev;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM,
-            (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2, 65535));
+  int64_t nb = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, (unsigned)std::min<int64_t>(nb, 65535));
   kern<<<grid, WARPS_M * WARPS_N * 32, smem, s>>>(g);
   count_launch();
   check_launch("dgemm_dmma_kernel");
 }
 
+template <int BM, int BN, int WM_, int WN_, int ST, bool V16>
+void launch_b(const Gemm& g, bool brow, cudaStream_t s) {
+  if (brow) launch_dmma<BM, BN, WM_, WN_, ST, true, V16>(g, s);
+  else launch_dmma<BM, BN, WM_, WN_, ST, false, V16>(g, s);
+}
+
+template <bool V16>
+void dispatch(const Gemm& g, bool brow, cudaStream_t s) {
+  const int64_t nb = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  const int64_t t128 = ((g.M + 127) / 128) * (int64_t)((g.N + 127) / 128) * nb;
+  const int64_t t12864 = ((g.M + 127) / 128) * (int64_t)((g.N + 63) / 64) * nb;
+  const int64_t t64 = ((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * nb;
+  static int variant = getenv("GPFVM_GEMM_VARIANT") ? atoi(getenv("GPFVM_GEMM_VARIANT")) : 1;
+  if (t128 >= 2 * 148 && variant == 0) launch_b<128, 128, 2, 4, 3, V16>(g, brow, s);
+  else if (t128 >= 2 * 148 && variant == 1) launch_b<128, 128, 4, 4, 3, V16>(g, brow, s);
+  else if (t128 >= 2 * 148 && variant == 2) launch_b<128, 128, 4, 4, 4, V16>(g, brow, s);
+  else if (t12864 >= 2 * 148) launch_b<128, 64, 4, 2, 3, V16>(g, brow, s);
+  else if (t64 >= 148) launch_b<64, 64, 2, 2, 3, V16>(g, brow, s);
+  else launch_b<32, 32, 2, 2, 4, V16>(g, brow, s);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool even(int64_t v) { return (v & 1) == 0; }
+
 }  // namespace
 
-double gemm_flops(const Gemm& g) { return 2.0 * g.M * (double)g.N * g.K * g.batch1 * g.batch2; }
+double gemm_flops(const Gemm& g) {
+  return 2.0 * g.M * (double)g.N * g.K * g.nseg * g.batch1 * g.batch2 * g.batch3;
+}
 
 void run_gemm(const Gemm& g, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0 || g.batch1 <= 0 || g.batch2 <= 0) return;
-  if (g.K <= 0) {
-    GPFVM_CHECK(false, GPFVM_ERR_INVALID, "run_gemm: K must be positive");
-  }
+  if (g.M <= 0 || g.N <= 0 || g.batch1 <= 0 || g.batch2 <= 0 || g.batch3 <= 0) return;
+  GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
-                    g.N >= 8 && g.K >= 4;
+                    g.N >= 8 && g.K * g.nseg >= 4;
   if (!fast) {
     int64_t total = (int64_t)g.M * g.N;
     int threads = 256;
     unsigned bx = (unsigned)std::min<int64_t>((total + threads - 1) / threads, 4096);
-    unsigned by = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2, 65535);
+    unsigned by = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
     dgemm_generic_kernel<<<dim3(bx, by), threads, 0, s>>>(g);
     count_launch();
     check_launch("dgemm_generic_kernel");
     return;
   }
   const bool brow = (g.b_cs == 1);
-  const int64_t nb = (int64_t)g.batch1 * g.batch2;
-  const int64_t tiles64 = ((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * nb;
-  const int64_t tiles128 = ((g.M + 127) / 128) * (int64_t)((g.N + 63) / 64) * nb;
-  if (tiles128 >= 4 * 148) {
-    if (brow) launch_dmma<128, 64, 4, 2, true>(g, s);
-    else launch_dmma<128, 64, 4, 2, false>(g, s);
-  } else if (tiles64 >= 2 * 148) {
-    if (brow) launch_dmma<64, 64, 2, 2, true>(g, s);
-    else launch_dmma<64, 64, 2, 2, false>(g, s);
-  } else {
-    if (brow) launch_dmma<32, 32, 2, 2, true>(g, s);
-    else launch_dmma<32, 32, 2, 2, false>(g, s);
-  }
+  const int64_t b_ld = brow ? g.b_rs : g.b_cs;
+  const bool v16 = aligned16(g.A) && aligned16(g.B) && even(g.a_rs) && even(b_ld) && even(g.a_b1) &&
+                   even(g.a_b2) && even(g.a_b3) && even(g.b_b1) && even(g.b_b2) && even(g.b_b3) &&
+                   even(g.a_sg) && even(g.b_sg);
+  if (v16) dispatch<true>(g, brow, s);
+  else dispatch<false>(g, brow, s);
 }
 
 }  // namespace gpfvm

@@ -83,16 +83,18 @@ void launch_factor(const MaternDD& K, const Sites& L, int mL, const Sites& R, in
                    int64_t ld, cudaStream_t s);
 
 // ---- GEMM ------------------------------------------------------------------------
-// C[b] = alpha * A[b] * B[b] + beta * C[b] for b = (b1, b2), element strides.
+// C[b] = alpha * sum_seg A_seg[b] * B_seg[b] + beta * C[b]; b = (b1, b2, b3),
+// element strides; A_seg = A + seg * a_sg, B_seg = B + seg * b_sg.
 struct Gemm {
   int M = 0, N = 0, K = 0;
-  int batch1 = 1, batch2 = 1;
+  int nseg = 1;
+  int batch1 = 1, batch2 = 1, batch3 = 1;
   const double* A = nullptr;
-  int64_t a_rs = 0, a_cs = 0, a_b1 = 0, a_b2 = 0;
+  int64_t a_rs = 0, a_cs = 0, a_b1 = 0, a_b2 = 0, a_b3 = 0, a_sg = 0;
   const double* B = nullptr;
-  int64_t b_rs = 0, b_cs = 0, b_b1 = 0, b_b2 = 0;
+  int64_t b_rs = 0, b_cs = 0, b_b1 = 0, b_b2 = 0, b_b3 = 0, b_sg = 0;
   double* C = nullptr;
-  int64_t c_rs = 0, c_cs = 0, c_b1 = 0, c_b2 = 0;
+  int64_t c_rs = 0, c_cs = 0, c_b1 = 0, c_b2 = 0, c_b3 = 0;
   double alpha = 1.0, beta = 0.0;
 };
 void run_gemm(const Gemm& g, cudaStream_t s);

@@ -1,5 +1,6 @@
 // C ABI: handle lifetime, factor assembly (§8 row 1) and the Kronecker Gram
 // matvec (§8 row 2).  See include/gpfvm.h for the contract and DESIGN.md §4.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -201,19 +202,134 @@ void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std
   }
 }
 
-void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
-  GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_gram_matvec: call gpfvm_assemble_factors first");
-  vec_scale_add(y, x, p->noise.ptr, p->N, nrhs, ld, s);
+MatvecPlan::~MatvecPlan() {
+  release_graphs();
+  for (auto st : branch) cudaStreamDestroy(st);
+  if (cap) cudaStreamDestroy(cap);
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+void MatvecPlan::release_graphs() {
+  for (auto& g : graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs.clear();
+}
+
+// One KronSum per nonzero block pair (built after the factors exist).
+void build_plan(gpfvm_problem* p, cudaStream_t s) {
+  auto plan = std::make_unique<MatvecPlan>();
   const int nb = (int)p->blocks.size();
+  plan->by_out.assign(nb, {});
   for (int I = 0; I < nb; I++)
     for (int J = 0; J < nb; J++) {
-      std::vector<const KronTerm*> ts;
-      for (const auto& t : p->terms)
-        if (t.I == I && t.J == J) ts.push_back(&t);
-      if (ts.empty()) continue;
-      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[I].shape, x + p->blocks[J].offset, ld,
-                  y + p->blocks[I].offset, ld, nrhs, false, s, p->ws);
+      std::vector<double> coefs;
+      std::vector<std::vector<const double*>> fs;
+      for (const auto& t : p->terms) {
+        if (t.I != I || t.J != J) continue;
+        coefs.push_back(t.coef);
+        std::vector<const double*> f;
+        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        fs.push_back(f);
+      }
+      if (coefs.empty()) continue;
+      PairOp op;
+      op.I = I;
+      op.J = J;
+      op.ks.build(p->ndim, p->blocks[J].shape, p->blocks[I].shape, coefs, fs, s);
+      plan->flops_per_rhs += op.ks.flops_per_rhs();
+      plan->by_out[I].push_back((int)plan->pairs.size());
+      plan->pairs.push_back(std::move(op));
     }
+  plan->w0.resize(nb);
+  plan->w1.resize(nb);
+  p->plan = std::move(plan);
+}
+
+static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
+  MatvecPlan& pl = *p->plan;
+  const BlockInt& B = p->blocks[I];
+  vec_scale_add(y + B.offset, x + B.offset, p->noise.ptr + B.offset, B.size, nrhs, ld, s);
+  for (int k : pl.by_out[I]) {
+    const PairOp& op = pl.pairs[k];
+    op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, 1.0, pl.w0[I].ptr, pl.w1[I].ptr, s);
+  }
+}
+
+static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
+  MatvecPlan& pl = *p->plan;
+  for (size_t I = 0; I < pl.by_out.size(); I++) {
+    int64_t need = 0;
+    for (int k : pl.by_out[I]) need = std::max(need, pl.pairs[k].ks.workspace_per_rhs());
+    size_t n = (size_t)std::max<int64_t>(1, need * nrhs);
+    if (pl.w0[I].n < n) {
+      pl.release_graphs();  // captured graphs reference the old buffers
+      pl.w0[I].ensure(n);
+      pl.w1[I].ensure(n);
+    }
+  }
+}
+
+// Y = G X (+ Sigma X).  Direct launch the first time a (x, y, nrhs, ld) key is
+// seen; from the second time on the whole matvec is a CUDA graph (one branch
+// per output block, joined) replayed on `s`.
+void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
+  GPFVM_CHECK(p->assembled && p->plan, GPFVM_ERR_STATE, "gpfvm_gram_matvec: call gpfvm_assemble_factors first");
+  MatvecPlan& pl = *p->plan;
+  ensure_plan_workspace(p, nrhs);
+  const int nb = (int)p->blocks.size();
+  static const bool no_graph = getenv("GPFVM_NO_GRAPH") != nullptr;
+  MatvecPlan::G* hit = nullptr;
+  for (auto& g : pl.graphs)
+    if (g.x == x && g.y == y && g.nrhs == nrhs && g.ld == ld) hit = &g;
+  if (hit && hit->exec) {
+    GPFVM_CUDA(cudaGraphLaunch(hit->exec, s));
+    count_launch(hit->nodes);
+    return;
+  }
+  if (no_graph || !hit) {
+    if (!no_graph) {
+      if (pl.graphs.size() >= 16) {
+        if (pl.graphs.front().exec) cudaGraphExecDestroy(pl.graphs.front().exec);
+        pl.graphs.erase(pl.graphs.begin());
+      }
+      pl.graphs.push_back({x, y, nrhs, ld, nullptr, 0, 1});
+    }
+    for (int I = 0; I < nb; I++) matvec_branch(p, I, x, y, nrhs, ld, s);
+    return;
+  }
+  // second sighting: capture
+  if (!pl.cap) {
+    GPFVM_CUDA(cudaStreamCreateWithFlags(&pl.cap, cudaStreamNonBlocking));
+    pl.branch.resize(nb);
+    for (int I = 0; I < nb; I++) GPFVM_CUDA(cudaStreamCreateWithFlags(&pl.branch[I], cudaStreamNonBlocking));
+    pl.ev.resize(nb + 1);
+    for (auto& e : pl.ev) GPFVM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int64_t l0 = g_launches.load();
+  cudaGraph_t graph;
+  GPFVM_CUDA(cudaStreamBeginCapture(pl.cap, cudaStreamCaptureModeThreadLocal));
+  try {
+    GPFVM_CUDA(cudaEventRecord(pl.ev[nb], pl.cap));
+    for (int I = 0; I < nb; I++) {
+      GPFVM_CUDA(cudaStreamWaitEvent(pl.branch[I], pl.ev[nb], 0));
+      matvec_branch(p, I, x, y, nrhs, ld, pl.branch[I]);
+      GPFVM_CUDA(cudaEventRecord(pl.ev[I], pl.branch[I]));
+      GPFVM_CUDA(cudaStreamWaitEvent(pl.cap, pl.ev[I], 0));
+    }
+  } catch (...) {
+    cudaStreamEndCapture(pl.cap, &graph);
+    throw;
+  }
+  GPFVM_CUDA(cudaStreamEndCapture(pl.cap, &graph));
+  cudaGraphExec_t exec;
+  GPFVM_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  const int64_t nodes = g_launches.load() - l0;
+  g_launches.fetch_sub(nodes);
+  hit->exec = exec;
+  hit->nodes = nodes;
+  GPFVM_CUDA(cudaGraphLaunch(exec, s));
+  count_launch(nodes);
 }
 
 }  // namespace gpfvm
@@ -309,6 +425,7 @@ int gpfvm_assemble_factors(gpfvm_problem* p, void* stream) {
     }
     p->noise.ensure(std::max<int64_t>(1, p->N));
     for (const auto& B : p->blocks) fill(p->noise.ptr + B.offset, B.noise, B.size, s);
+    build_plan(p, s);
     p->assembled = true;
     destroy_precond(p->pc);  // factors changed: rebuild lazily
     p->pc = nullptr;
@@ -369,6 +486,7 @@ int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, in
 
 double gpfvm_matvec_flops(const gpfvm_problem* p) {
   if (!p) return 0.0;
+  if (p->plan) return p->plan->flops_per_rhs;
   double fl = 0.0;
   for (const auto& t : p->terms) fl += term_flops(p, t, p->blocks[t.J].shape, p->blocks[t.I].shape);
   return fl;

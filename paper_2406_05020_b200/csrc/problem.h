@@ -58,6 +58,49 @@ struct Workspace {
   DevBuf t0, t1;
 };
 
+// Fused sum of Kronecker products of one block pair (kron.cu)
+struct KronSum {
+  int d = 0, P = 0;
+  int nin[GPFVM_MAX_DIMS] = {1, 1, 1, 1}, nout[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
+  DevBuf stk[GPFVM_MAX_DIMS];  // stacked factors per dim (coefficients folded into dim 0)
+  void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
+             const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
+  int64_t workspace_per_rhs() const;
+  double flops_per_rhs() const;
+  // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
+  void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
+             cudaStream_t s) const;
+};
+
+struct PairOp {
+  int I = 0, J = 0;
+  KronSum ks;
+};
+
+// Matvec plan: one KronSum per nonzero block pair, grouped by output block
+// (graph branches), with CUDA-graph replay cached per (x, y, nrhs, ld).
+struct MatvecPlan {
+  std::vector<PairOp> pairs;
+  std::vector<std::vector<int>> by_out;
+  std::vector<DevBuf> w0, w1;  // per output-block branch
+  std::vector<cudaStream_t> branch;
+  cudaStream_t cap = nullptr;
+  std::vector<cudaEvent_t> ev;
+  struct G {
+    const double* x;
+    double* y;
+    int nrhs;
+    int64_t ld;
+    cudaGraphExec_t exec;
+    int64_t nodes;
+    int seen;
+  };
+  std::vector<G> graphs;
+  double flops_per_rhs = 0.0;
+  ~MatvecPlan();
+  void release_graphs();
+};
+
 }  // namespace gpfvm
 
 struct gpfvm_problem {
@@ -75,6 +118,8 @@ struct gpfvm_problem {
   gpfvm::Precond* pc = nullptr;
   gpfvm::Krylov kry;
   gpfvm::DevBuf stage_in, stage_out;  // host-pointer staging
+  std::unique_ptr<gpfvm::MatvecPlan> plan;
+  gpfvm::DevBuf pcg_s, pcg_z;           // fixed PCG operands (graph-replayable matvec)
   ~gpfvm_problem();
 };
 
@@ -88,6 +133,7 @@ void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std
                  const int* out_shape, const double* x, int64_t ldx, double* y, int64_t ldy, int R,
                  bool overwrite, cudaStream_t s, Workspace& ws);
 void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s);
+void build_plan(gpfvm_problem* p, cudaStream_t s);
 double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape);
 int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr);
 

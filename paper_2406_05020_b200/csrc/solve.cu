@@ -396,9 +396,15 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
     ensure_krylov(p, K.k + 1, s);
     double* d = K.d.ptr + (int64_t)K.k * N;
     double* gd = K.gd.ptr + (int64_t)K.k * N;
-    if (p->pc) precond_apply(p, r.ptr, d, s);
-    else copy(d, r.ptr, N, s);
-    matvec_device(p, d, gd, 1, N, s);  // z = G s (stored in gd)
+    // s = P^{-1} r ; z = G s  on fixed operands (graph-replayed matvec), then
+    // copied into the Krylov slots
+    p->pcg_s.ensure(N);
+    p->pcg_z.ensure(N);
+    if (p->pc) precond_apply(p, r.ptr, p->pcg_s.ptr, s);
+    else copy(p->pcg_s.ptr, r.ptr, N, s);
+    matvec_device(p, p->pcg_s.ptr, p->pcg_z.ptr, 1, N, s);
+    copy(d, p->pcg_s.ptr, N, s);
+    copy(gd, p->pcg_z.ptr, N, s);
     if (K.k > 0) {
       // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j
       dot_many(K.d.ptr, N, gd, N, K.k, dsc, s);
