@@ -238,6 +238,39 @@ __global__ void dgemm_generic_kernel(Gemm g) {
   }
 }
 
+// Skinny fallback (few outputs, long K): one warp per C entry, lanes stride K
+// (coalesced when A is row-major or B column-major), shuffle reduction.
+__global__ void dgemm_skinny_kernel(Gemm g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps_per_block = blockDim.x >> 5;
+  const int64_t total = (int64_t)g.M * g.N;
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  for (int64_t z = blockIdx.y; z < nbatch; z += gridDim.y) {
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3;
+    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3;
+    for (int64_t idx = blockIdx.x * warps_per_block + (threadIdx.x >> 5); idx < total;
+         idx += (int64_t)gridDim.x * warps_per_block) {
+      const int m = (int)(idx / g.N), n = (int)(idx % g.N);
+      double acc = 0.0;
+      for (int seg = 0; seg < g.nseg; seg++) {
+        const double* Ar = A + seg * g.a_sg + (int64_t)m * g.a_rs;
+        const double* Bc = B + seg * g.b_sg + (int64_t)n * g.b_cs;
+        for (int k = lane; k < g.K; k += 32) acc = fma(Ar[k * g.a_cs], Bc[k * g.b_rs], acc);
+      }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        double* cp = C + (int64_t)m * g.c_rs + (int64_t)n * g.c_cs;
+        double v = g.alpha * acc;
+        if (g.beta != 0.0) v += g.beta * *cp;
+        *cp = v;
+      }
+    }
+  }
+}
+
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool B_ROW, bool V16>
 void launch_dmma(const Gemm& g, cudaStream_t s) {
   using L = SmemLayout<BM, BN, B_ROW>;
@@ -294,6 +327,16 @@ void run_gemm(const Gemm& g, cudaStream_t s) {
                     g.N >= 8 && g.K * g.nseg >= 4;
   if (!fast) {
     int64_t total = (int64_t)g.M * g.N;
+    const int64_t kk = (int64_t)g.K * g.nseg;
+    if (kk >= 32 && total <= (1 << 20)) {
+      const int threads = 256;  // 8 warps, one output each
+      unsigned bx = (unsigned)std::min<int64_t>((total + 7) / 8, 4096);
+      unsigned by = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
+      dgemm_skinny_kernel<<<dim3(bx, by), threads, 0, s>>>(g);
+      count_launch();
+      check_launch("dgemm_skinny_kernel");
+      return;
+    }
     int threads = 256;
     unsigned bx = (unsigned)std::min<int64_t>((total + threads - 1) / threads, 4096);
     unsigned by = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);

@@ -61,6 +61,7 @@ struct Workspace {
 // Fused sum of Kronecker products of one block pair (kron.cu)
 struct KronSum {
   int d = 0, P = 0;
+  bool rev = false;  // contraction order: dim d-1 first (chosen by flop count)
   int nin[GPFVM_MAX_DIMS] = {1, 1, 1, 1}, nout[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
   DevBuf stk[GPFVM_MAX_DIMS];  // stacked factors per dim (coefficients folded into dim 0)
   void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
