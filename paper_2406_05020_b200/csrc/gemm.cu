@@ -213,24 +213,25 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
 
 // Generic strided fallback (tiny / irregular shapes): one thread per C entry.
 __global__ void dgemm_generic_kernel(Gemm g) {
-  const int64_t total = (int64_t)g.M * g.N;
+  // 2D mapping without 64-bit divisions: x covers columns n (coalesced for
+  // row-major B/C), y loops rows m; z covers the batch.
   const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
-  for (int64_t z = blockIdx.y; z < nbatch; z += gridDim.y) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.N) return;
+  for (int64_t z = blockIdx.z; z < nbatch; z += gridDim.z) {
     const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
     const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
     const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
     const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3;
     double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-      int m = (int)(idx / g.N), n = (int)(idx % g.N);
+    for (int m = blockIdx.y; m < g.M; m += gridDim.y) {
       double acc = 0.0;
       for (int seg = 0; seg < g.nseg; seg++) {
-        const double* As = A + seg * g.a_sg;
-        const double* Bs = B + seg * g.b_sg;
-        for (int k = 0; k < g.K; k++) acc = fma(As[m * g.a_rs + k * g.a_cs], Bs[k * g.b_rs + n * g.b_cs], acc);
+        const double* As = A + seg * g.a_sg + (int64_t)m * g.a_rs;
+        const double* Bs = B + seg * g.b_sg + (int64_t)n * g.b_cs;
+        for (int k = 0; k < g.K; k++) acc = fma(As[k * g.a_cs], Bs[k * g.b_rs], acc);
       }
-      double* cp = C + m * g.c_rs + n * g.c_cs;
+      double* cp = C + (int64_t)m * g.c_rs + (int64_t)n * g.c_cs;
       double v = g.alpha * acc;
       if (g.beta != 0.0) v += g.beta * *cp;
       *cp = v;
@@ -298,16 +299,18 @@ void launch_b(const Gemm& g, bool brow, cudaStream_t s) {
 
 template <bool V16>
 void dispatch(const Gemm& g, bool brow, cudaStream_t s) {
+  // Tile choice (measured on B200, tools/gemm_bench.cu): 128x64 CTA tiles
+  // with 8 warps of 32x32 (2 CTAs/SM) give the best DMMA throughput for the
+  // mode-product shapes (~28-30 TF/s of 37); smaller tiles when the grid would
+  // not fill the 148 SMs.
   const int64_t nb = (int64_t)g.batch1 * g.batch2 * g.batch3;
-  const int64_t t128 = ((g.M + 127) / 128) * (int64_t)((g.N + 127) / 128) * nb;
   const int64_t t12864 = ((g.M + 127) / 128) * (int64_t)((g.N + 63) / 64) * nb;
   const int64_t t64 = ((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * nb;
-  static int variant = getenv("GPFVM_GEMM_VARIANT") ? atoi(getenv("GPFVM_GEMM_VARIANT")) : 1;
-  if (t128 >= 2 * 148 && variant == 0) launch_b<128, 128, 2, 4, 3, V16>(g, brow, s);
-  else if (t128 >= 2 * 148 && variant == 1) launch_b<128, 128, 4, 4, 3, V16>(g, brow, s);
-  else if (t128 >= 2 * 148 && variant == 2) launch_b<128, 128, 4, 4, 4, V16>(g, brow, s);
-  else if (t12864 >= 2 * 148) launch_b<128, 64, 4, 2, 3, V16>(g, brow, s);
-  else if (t64 >= 148) launch_b<64, 64, 2, 2, 3, V16>(g, brow, s);
+  static const int variant = getenv("GPFVM_GEMM_VARIANT") ? atoi(getenv("GPFVM_GEMM_VARIANT")) : -1;
+  if (variant == 0) { launch_b<128, 128, 2, 4, 3, V16>(g, brow, s); return; }
+  if (variant == 3) { launch_b<64, 32, 2, 2, 4, V16>(g, brow, s); return; }
+  if (t12864 >= 148) launch_b<128, 64, 4, 2, 3, V16>(g, brow, s);
+  else if (t64 >= 148) launch_b<64, 64, 2, 2, 4, V16>(g, brow, s);
   else launch_b<32, 32, 2, 2, 4, V16>(g, brow, s);
 }
 
@@ -320,7 +323,17 @@ double gemm_flops(const Gemm& g) {
   return 2.0 * g.M * (double)g.N * g.K * g.nseg * g.batch1 * g.batch2 * g.batch3;
 }
 
-void run_gemm(const Gemm& g, cudaStream_t s) {
+void run_gemm(const Gemm& g0, cudaStream_t s) {
+  Gemm g = g0;
+  // A single-row GEMM batched over right-hand sides that share B is one GEMM
+  // with the batch as its M dimension (e.g. IC-block contractions).
+  if (g.M == 1 && g.batch1 > 1 && g.batch2 == 1 && g.batch3 == 1 && g.b_b1 == 0) {
+    g.M = g.batch1;
+    g.a_rs = g.a_b1;
+    g.c_rs = g.c_b1;
+    g.batch1 = 1;
+    g.a_b1 = g.c_b1 = 0;
+  }
   if (g.M <= 0 || g.N <= 0 || g.batch1 <= 0 || g.batch2 <= 0 || g.batch3 <= 0) return;
   GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
@@ -337,10 +350,11 @@ void run_gemm(const Gemm& g, cudaStream_t s) {
       check_launch("dgemm_skinny_kernel");
       return;
     }
-    int threads = 256;
-    unsigned bx = (unsigned)std::min<int64_t>((total + threads - 1) / threads, 4096);
-    unsigned by = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
-    dgemm_generic_kernel<<<dim3(bx, by), threads, 0, s>>>(g);
+    const int threads = g.N >= 128 ? 128 : 32;
+    unsigned bx = (unsigned)((g.N + threads - 1) / threads);
+    unsigned by = (unsigned)std::min(g.M, 16);  // each thread loops over several rows
+    unsigned bz = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
+    dgemm_generic_kernel<<<dim3(bx, by, bz), threads, 0, s>>>(g);
     count_launch();
     check_launch("dgemm_generic_kernel");
     return;

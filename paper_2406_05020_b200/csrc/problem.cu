@@ -248,10 +248,14 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
 static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
   MatvecPlan& pl = *p->plan;
   const BlockInt& B = p->blocks[I];
-  vec_scale_add(y + B.offset, x + B.offset, p->noise.ptr + B.offset, B.size, nrhs, ld, s);
+  // noise-free block: the first pair overwrites (beta = 0), saving one read-modify-write pass
+  bool overwrite = (B.noise == 0.0) && !pl.by_out[I].empty();
+  if (!overwrite) vec_scale_add(y + B.offset, x + B.offset, p->noise.ptr + B.offset, B.size, nrhs, ld, s);
   for (int k : pl.by_out[I]) {
     const PairOp& op = pl.pairs[k];
-    op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, 1.0, pl.w0[I].ptr, pl.w1[I].ptr, s);
+    op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr,
+                pl.w1[I].ptr, s);
+    overwrite = false;
   }
 }
 
