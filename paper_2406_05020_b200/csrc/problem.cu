@@ -217,6 +217,23 @@ void MatvecPlan::release_graphs() {
 
 // One KronSum per nonzero block pair (built after the factors exist).
 void build_plan(gpfvm_problem* p, cudaStream_t s) {
+  if (p->plan) {
+    // re-assembly of the same problem: refresh the stacked factors in place
+    // (same shapes -> same buffers), so captured matvec graphs stay valid
+    for (auto& op : p->plan->pairs) {
+      std::vector<double> coefs;
+      std::vector<std::vector<const double*>> fs;
+      for (const auto& t : p->terms) {
+        if (t.I != op.I || t.J != op.J) continue;
+        coefs.push_back(t.coef);
+        std::vector<const double*> f;
+        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        fs.push_back(f);
+      }
+      op.ks.build(p->ndim, p->blocks[op.J].shape, p->blocks[op.I].shape, coefs, fs, s);
+    }
+    return;
+  }
   auto plan = std::make_unique<MatvecPlan>();
   const int nb = (int)p->blocks.size();
   plan->by_out.assign(nb, {});

@@ -16,6 +16,8 @@
 //   Gd = z - sum c_j Gd_j ; eta = z.d ; a = d.r / eta ; x += a d ; r -= a Gd
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "problem.h"
 
@@ -77,6 +79,20 @@ __global__ void symm_kernel(double* A, int n) {
   A[(int64_t)r * n + c] = v;
   A[(int64_t)c * n + r] = v;
 }
+
+struct PhaseTimer {
+  cudaStream_t s;
+  bool on;
+  double t0;
+  explicit PhaseTimer(cudaStream_t st) : s(st), on(getenv("GPFVM_DEBUG") != nullptr), t0(0) { mark(nullptr); }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (what) fprintf(stderr, "[gpfvm] %-28s %8.2f ms\n", what, t - t0);
+    t0 = t;
+  }
+};
 
 unsigned g1(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
@@ -211,6 +227,8 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
                   S.ptr + pc.boff[jb] * nb + pc.boff[ib], nb, nJ, true, s, p->ws);
     }
   }
+  PhaseTimer pt(s);
+  pt.mark("ldl: Gpb/Gbb from identities");
   // noise on the diagonal of G_bb
   {
     std::vector<double> nz(nb);
@@ -227,6 +245,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   }
   // Y^T = FD(G_pb) rows
   fd_apply(pc, pc.GpbT.ptr, np, pc.YT.ptr, np, nb, s);
+  pt.mark("ldl: Y = FD(Gpb)");
   // S = G_bb - G_pb^T Y
   {
     Gemm g;
@@ -239,6 +258,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   }
   symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(S.ptr, nb);
   count_launch();
+  pt.mark("ldl: S = Gbb - Gpb^T Y");
   // Cholesky with shift-on-failure
   S0.ensure((size_t)nb * nb);
   Lf.ensure((size_t)nb * nb);
@@ -275,7 +295,9 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   pc.Sinv.ensure((size_t)nb * nb);
   set_identity_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb, nb);
   count_launch();
+  pt.mark("ldl: cholesky(S)");
   cholesky_solve(Lf.ptr, nb, pc.Sinv.ptr, nb, s);
+  pt.mark("ldl: S^{-1}");
   symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb);
   count_launch();
   pc.rb.ensure(nb);
@@ -304,7 +326,9 @@ static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
       }
     }
     GPFVM_CHECK(pc->P >= 0, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: no non-deflated (PDE) block");
+    PhaseTimer pt(s);
     build_fd(p, *pc, s);
+    pt.mark("fd: 2 x sygv");
     build_ldl(p, *pc, s);
   } catch (...) {
     delete pc;
