@@ -140,6 +140,49 @@ int gpfvm_factor_matrix(const gpfvm_kernel1d* k, const gpfvm_sites1d* left, int 
 int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld,
                       void* stream);
 
+/* General Kronecker-sum primitive (the local kernel of the sharded path,
+ * DESIGN.md §7):  Y_r = beta*Y_r + sum_p c_p ((x)_{i<ndim} F_{p,i}) X_r  for
+ * r < nrhs, with X_r/Y_r tensors of shape in_shape / out_shape flattened
+ * row-major (dim 0 slowest).  factors[p*ndim + i] is a DEVICE pointer to the
+ * row-major out_shape[i] x in_shape[i] matrix F_{p,i}.  x, y: DEVICE pointers,
+ * must not alias.  Same fused plan as gpfvm_gram_matvec (d DMMA GEMMs). */
+int gpfvm_kron_matvec(int ndim, const int* in_shape, const int* out_shape, int n_terms, const double* coefs,
+                      const double* const* factors, const double* x, int64_t ldx, double* y, int64_t ldy,
+                      int nrhs, double beta, void* stream);
+
+/* Row-major DMMA GEMM  C = alpha A B + beta C  (A: M x K, B: K x N, C: M x N;
+ * DEVICE pointers, leading dimensions in elements).  The time contraction of
+ * the sharded path after its all-to-all. */
+int gpfvm_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double beta, double* C, int64_t ldc, void* stream);
+
+/* dst = permutation of the row-major tensor src (ndim <= 4): dst has shape
+ * (shape[perm[0]], ..., shape[perm[ndim-1]]).  DEVICE pointers, no aliasing. */
+int gpfvm_permute(int ndim, const int* shape, const int* perm, const double* src, double* dst, void* stream);
+
+/* Generalised symmetric-definite eigenproblem  A V = B V diag(w),  V^T B V = I
+ * (A symmetric, B SPD; n x n row-major DEVICE matrices; V row-major with the
+ * eigenvectors in its columns).  Cholesky reduction + one-sided block Jacobi
+ * (DESIGN.md §5.1).  Synchronises `stream`. */
+int gpfvm_sygv(int n, const double* A, const double* B, double* V, double* w, void* stream);
+
+/* Fused solver vector ops (DEVICE pointers; coef is a DEVICE array of k values):
+ *   gpfvm_dot_many:  out[j] = X_j . v  for j < k (X_j = X + j*ldx), warp-shuffle
+ *                    reductions, deterministic fixed-order second pass
+ *   gpfvm_axpy_many: y += sign * sum_j coef[j] X_j  (one pass over y) */
+int gpfvm_dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, double* out, void* stream);
+int gpfvm_axpy_many(double* y, const double* X, int64_t ldx, const double* coef, double sign, int64_t n, int k,
+                    void* stream);
+
+/* Fast-diagonalisation factors of a two-term 2D Kronecker block
+ * ca A0(x)A1 + cb B0(x)B1 (+ noise I):  B0 V = A0 V Lam,
+ * A1 W = B1 W M,  Dinv[i*n1+j] = 1/(ca M_j + cb Lam_i + noise |v_i|^2 |w_j|^2).
+ * All DEVICE row-major; V n0 x n0, W n1 x n1, Dinv n0*n1.  Synchronises. */
+int gpfvm_fd_setup(int n0, int n1, const double* A0, const double* A1, const double* B0, const double* B1,
+                   double ca, double cb, double noise, double* V, double* W, double* Dinv, void* stream);
+/* x[i] *= d[i]  (DEVICE pointers) */
+int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream);
+
 /* ---- §8 row 3: solve -----------------------------------------------------
  * Solve G alpha = y with preconditioned CG in IterGP form (§4.1; Wenger et
  * al. 2022 Alg. 1, CG policy, full reorthogonalisation §6 l.475): actions

@@ -70,6 +70,20 @@ EXPORTS = {
                               C.POINTER(SolveReport), C.c_void_p]),
     "gpfvm_predict": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                 C.c_void_p]),
+    "gpfvm_kron_matvec": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double),
+                                    C.POINTER(C.c_void_p), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
+                                    C.c_double, C.c_void_p]),
+    "gpfvm_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                             C.c_double, C.c_void_p, C.c_int64, C.c_void_p]),
+    "gpfvm_permute": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
+    "gpfvm_sygv": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_dot_many": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p]),
+    "gpfvm_axpy_many": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double, C.c_int64, C.c_int,
+                                  C.c_void_p]),
+    "gpfvm_fd_setup": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                 C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_vmul": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "gpfvm_launch_count": (C.c_int64, []),
     "gpfvm_matvec_flops": (C.c_double, [C.c_void_p]),
 }

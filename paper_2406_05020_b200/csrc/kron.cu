@@ -202,3 +202,68 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
 }
 
 }  // namespace gpfvm
+
+// ---- C ABI: standalone Kronecker-sum matvec ------------------------------------
+namespace gpfvm {
+int guarded_kron(int ndim, const int* in_shape, const int* out_shape, int P, const double* coefs,
+                 const double* const* factors, const double* x, int64_t ldx, double* y, int64_t ldy, int R,
+                 double beta, cudaStream_t s) {
+  try {
+    GPFVM_CHECK(ndim >= 1 && ndim <= GPFVM_MAX_DIMS && P >= 0 && R >= 1, GPFVM_ERR_INVALID, "bad kron_matvec sizes");
+    GPFVM_CHECK(in_shape && out_shape && (P == 0 || (coefs && factors)) && x && y, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(x != y, GPFVM_ERR_INVALID, "x and y must not alias");
+    int64_t nin = 1, nout = 1;
+    for (int i = 0; i < ndim; i++) {
+      GPFVM_CHECK(in_shape[i] >= 1 && out_shape[i] >= 1, GPFVM_ERR_INVALID, "empty dimension");
+      nin *= in_shape[i];
+      nout *= out_shape[i];
+    }
+    GPFVM_CHECK(ldx >= nin && ldy >= nout, GPFVM_ERR_INVALID, "ld smaller than the tensor size");
+    std::vector<double> c(coefs, coefs + P);
+    std::vector<std::vector<const double*>> fs(P);
+    for (int p = 0; p < P; p++) fs[p].assign(factors + p * ndim, factors + (p + 1) * ndim);
+    // cached plan + workspace keyed on the factor pointers (thread-local, small LRU)
+    struct Entry {
+      std::vector<int> key_shape;
+      std::vector<double> key_c;
+      std::vector<const double*> key_f;
+      std::unique_ptr<KronSum> ks;
+    };
+    static thread_local std::vector<Entry> cache;
+    static thread_local DevBuf w0, w1;
+    std::vector<int> ks_shape(in_shape, in_shape + ndim);
+    ks_shape.insert(ks_shape.end(), out_shape, out_shape + ndim);
+    std::vector<const double*> kf(factors, factors + (size_t)P * ndim);
+    KronSum* ks = nullptr;
+    for (auto& e : cache)
+      if (e.key_shape == ks_shape && e.key_c == c && e.key_f == kf) ks = e.ks.get();
+    if (!ks) {
+      if (cache.size() >= 8) cache.erase(cache.begin());
+      Entry e{ks_shape, c, kf, std::make_unique<KronSum>()};
+      e.ks->build(ndim, in_shape, out_shape, c, fs, s);
+      ks = e.ks.get();
+      cache.push_back(std::move(e));
+    } else {
+      ks->build(ndim, in_shape, out_shape, c, fs, s);  // refresh contents (factors may have changed)
+    }
+    size_t need = (size_t)std::max<int64_t>(1, ks->workspace_per_rhs() * R);
+    w0.ensure(need);
+    w1.ensure(need);
+    ks->apply(x, ldx, y, ldy, R, beta, w0.ptr, w1.ptr, s);
+    return GPFVM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GPFVM_ERR_INVALID;
+  }
+}
+}  // namespace gpfvm
+
+extern "C" int gpfvm_kron_matvec(int ndim, const int* in_shape, const int* out_shape, int n_terms, const double* coefs,
+                                 const double* const* factors, const double* x, int64_t ldx, double* y, int64_t ldy,
+                                 int nrhs, double beta, void* stream) {
+  return gpfvm::guarded_kron(ndim, in_shape, out_shape, n_terms, coefs, factors, x, ldx, y, ldy, nrhs, beta,
+                             (cudaStream_t)stream);
+}

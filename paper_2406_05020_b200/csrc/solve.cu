@@ -472,3 +472,51 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
 }
 
 }  // namespace gpfvm
+
+// ---- C ABI: standalone FD setup and elementwise product (sharded path) ----------
+namespace gpfvm {
+namespace {
+__global__ void vmul_kernel(double* x, const double* __restrict__ d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] *= d[i];
+}
+}  // namespace
+}  // namespace gpfvm
+
+extern "C" int gpfvm_fd_setup(int n0, int n1, const double* A0, const double* A1, const double* B0, const double* B1,
+                              double ca, double cb, double noise, double* V, double* W, double* Dinv, void* stream) {
+  using namespace gpfvm;
+  try {
+    GPFVM_CHECK(n0 >= 1 && n1 >= 1 && A0 && A1 && B0 && B1 && V && W && Dinv, GPFVM_ERR_INVALID, "bad fd_setup args");
+    cudaStream_t s = (cudaStream_t)stream;
+    DevBuf lam, mu, vv, ww;
+    lam.ensure(n0); mu.ensure(n1); vv.ensure(n0); ww.ensure(n1);
+    sygv(B0, A0, n0, V, lam.ptr, s);
+    sygv(A1, B1, n1, W, mu.ptr, s);
+    colsumsq_kernel<<<g1(n0, 128), 128, 0, s>>>(V, n0, vv.ptr);
+    colsumsq_kernel<<<g1(n1, 128), 128, 0, s>>>(W, n1, ww.ptr);
+    dinv_kernel<<<g1((int64_t)n0 * n1), 256, 0, s>>>(Dinv, lam.ptr, mu.ptr, vv.ptr, ww.ptr, n0, n1, ca, cb, noise);
+    count_launch(3);
+    check_launch("gpfvm_fd_setup");
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    return GPFVM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  }
+}
+
+extern "C" int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream) {
+  using namespace gpfvm;
+  try {
+    GPFVM_CHECK(x && d && n >= 0, GPFVM_ERR_INVALID, "bad vmul args");
+    if (n == 0) return GPFVM_OK;
+    vmul_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 2048), 256, 0, (cudaStream_t)stream>>>(x, d, n);
+    count_launch();
+    check_launch("vmul_kernel");
+    return GPFVM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  }
+}
