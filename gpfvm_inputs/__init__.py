@@ -204,6 +204,142 @@ def heat_grid(nt: int, nx: int) -> Grid:
     return Grid([np.linspace(0.0, 1.0, nt), np.linspace(0.0, 1.0, nx)], 0)
 
 
+def _gauss_cell_integrals(lo, hi, c, w):
+    """int_lo^hi exp(-(x-c)^2 / (2 w^2)) dx (closed form with erf)."""
+    from scipy.special import erf
+    s = np.sqrt(2.0) * w
+    return w * np.sqrt(np.pi / 2.0) * (erf((hi - c) / s) - erf((lo - c) / s))
+
+
+def _face_blocks(T, X, Y, ht, hx, hy, terms_for_face, jitter, deflate=True):
+    """Four spatial boundary faces of a [0,1]^2 domain as FVM-style cell blocks:
+    x=0 / x=1: (t cells) x point x (y cells);  y=0 / y=1: (t cells) x (x cells) x point y."""
+    out = []
+    for name, sites, h in [("BCx0", [T, point(0.0), Y], hy), ("BCx1", [T, point(1.0), Y], hy),
+                           ("BCy0", [T, X, point(0.0)], hx), ("BCy1", [T, X, point(1.0)], hx)]:
+        n = sites[0].n * sites[1].n * sites[2].n
+        out.append(Block(name, sites, terms_for_face(name), jitter * (ht * h) ** 2, deflate, np.zeros(n)))
+    return out
+
+
+def wave_problem(nt: int, nx: int, ny: int, *, c: float = 1.0, ell=(0.1, 0.05, 0.05), q: int = 3,
+                 centers=None, width: float = 0.05, seed: int = 2, jitter: float = 1e-8,
+                 name: str | None = None) -> Problem:
+    """BASELINE config 2: u_tt = c^2 (u_xx + u_yy) on [0,1] x [0,1]^2, Matérn-7/2.
+    IC cells: u(0,.) = Gaussian bump (seeded centre, width 0.05) and u_t(0,.) = 0;
+    Dirichlet-0 BC cells on the four faces.  `centers` (k x 2) gives a k-RHS
+    batch (the bump centres); the problem's rhs() is the first one, all k are
+    in meta['rhs_batch']."""
+    rng = np.random.default_rng(seed)
+    if centers is None:
+        centers = rng.uniform(0.3, 0.7, size=(4, 2))
+    T, X, Y = cells(nt), cells(nx), cells(ny)
+    ht, hx, hy = 1.0 / nt, 1.0 / nx, 1.0 / ny
+    ic_vals = [np.outer(_gauss_cell_integrals(X.lo, X.hi, cx, width),
+                        _gauss_cell_integrals(Y.lo, Y.hi, cy, width)).ravel() for cx, cy in centers]
+    blocks = [
+        Block("IC_u", [point(0.0), X, Y], [Term(1.0, (0, 0, 0))], jitter * (hx * hy) ** 2, True, ic_vals[0]),
+        Block("IC_ut", [point(0.0), X, Y], [Term(1.0, (1, 0, 0))], jitter * (hx * hy) ** 2, True,
+              np.zeros(nx * ny)),
+    ]
+    blocks += _face_blocks(T, X, Y, ht, hx, hy, lambda f: [Term(1.0, (0, 0, 0))], jitter)
+    blocks.append(Block("PDE", [T, X, Y], [Term(1.0, (2, 0, 0)), Term(-c * c, (0, 2, 0)), Term(-c * c, (0, 0, 2))],
+                        0.0, False, np.zeros(nt * nx * ny)))
+    kern = [[Kernel1D(q, ell[0]), Kernel1D(q, ell[1]), Kernel1D(q, ell[2])]]
+    p = Problem(name or f"wave2d_{nt}x{nx}x{ny}", 3, kern, blocks, meta=dict(kind="wave2d", c=c, centers=centers))
+    rhs_batch = []
+    for v in ic_vals:
+        rhs_batch.append(np.concatenate([v] + [b.rhs for b in blocks[1:]]))
+    p.meta["rhs_batch"] = np.stack(rhs_batch)
+    return p
+
+
+def config2() -> Problem:
+    """BASELINE.json configs[2]: 64 x 128 x 128 cells (~1.05M FVM obs), 4-RHS batch."""
+    return wave_problem(64, 128, 128, name="config2_wave2d_64x128x128")
+
+
+def advdiff_problem(nt: int, nx: int, ny: int, *, a=(1.0, 0.5), eps: float = 0.01, ell=(0.2, 0.1, 0.1),
+                    q: int = 2, n_modes: int = 32, seed: int = 3, jitter: float = 1e-8,
+                    name: str | None = None) -> Problem:
+    """BASELINE config 3: u_t + a.grad u = eps Lap u on [0,1] x [0,1]^2, Matérn-5/2,
+    seeded random-Fourier IC (n_modes sine modes, amplitudes ~ N(0, 1/|k|^2)),
+    Dirichlet-0 BC cells."""
+    rng = np.random.default_rng(seed)
+    T, X, Y = cells(nt), cells(nx), cells(ny)
+    ht, hx, hy = 1.0 / nt, 1.0 / nx, 1.0 / ny
+    ks = rng.integers(1, 9, size=(n_modes, 2))
+    amp = rng.standard_normal(n_modes) / np.sqrt((ks ** 2).sum(1))
+    ix = lambda k, S: (np.cos(k * np.pi * S.lo) - np.cos(k * np.pi * S.hi)) / (k * np.pi)
+    ic = sum(A * np.outer(ix(k1, X), ix(k2, Y)) for A, (k1, k2) in zip(amp, ks)).ravel()
+    blocks = [Block("IC", [point(0.0), X, Y], [Term(1.0, (0, 0, 0))], jitter * (hx * hy) ** 2, True, ic)]
+    blocks += _face_blocks(T, X, Y, ht, hx, hy, lambda f: [Term(1.0, (0, 0, 0))], jitter)
+    blocks.append(Block("PDE", [T, X, Y], [Term(1.0, (1, 0, 0)), Term(a[0], (0, 1, 0)), Term(a[1], (0, 0, 1)),
+                                         Term(-eps, (0, 2, 0)), Term(-eps, (0, 0, 2))],
+                        0.0, False, np.zeros(nt * nx * ny)))
+    kern = [[Kernel1D(q, ell[0]), Kernel1D(q, ell[1]), Kernel1D(q, ell[2])]]
+    return Problem(name or f"advdiff2d_{nt}x{nx}x{ny}", 3, kern, blocks, meta=dict(kind="advdiff2d", a=a, eps=eps))
+
+
+def config3() -> Problem:
+    """BASELINE.json configs[3]: 128 x 256 x 256 cells (~8.4M FVM obs)."""
+    return advdiff_problem(128, 256, 256, name="config3_advdiff2d_128x256x256")
+
+
+def shallow_water_problem(nt: int, nx: int, ny: int, *, g: float = 9.81, H: float = 1.0,
+                          ell=(0.2, 0.1, 0.1), q: int = 2, width: float = 0.08, noise_frac: float = 0.01,
+                          seed: int = 4, jitter: float = 1e-8, name: str | None = None) -> Problem:
+    """BASELINE config 4: linearised constant-depth shallow water (PAPER.md
+    Eqs. 24-26 with f = k = 0, constant H):
+        eta_t + H (u_x + v_y) = 0,   u_t + g eta_x = 0,   v_t + g eta_y = 0
+    three outputs (eta, u, v) with independent Matérn-5/2 product priors
+    (Eq. 17); per output the same cell grid.  IC cells: eta = seeded Gaussian
+    displacement with 1% i.i.d. Gaussian observation noise (noise variance =
+    (0.01 std(eta_IC))^2, values perturbed with the same draw), u = v = 0.
+    Radiation BC cells on the four faces (App. C.4, P:l.757-761):
+    eta_t -/+ c eta_n = 0 with c = sqrt(g H), sign per outward normal."""
+    rng = np.random.default_rng(seed)
+    T, X, Y = cells(nt), cells(nx), cells(ny)
+    ht, hx, hy = 1.0 / nt, 1.0 / nx, 1.0 / ny
+    cx, cy = rng.uniform(0.35, 0.65, size=2)
+    eta0 = np.outer(_gauss_cell_integrals(X.lo, X.hi, cx, width), _gauss_cell_integrals(Y.lo, Y.hi, cy, width)).ravel()
+    sd = noise_frac * float(np.std(eta0))
+    eta_obs = eta0 + sd * rng.standard_normal(eta0.shape)
+    ETA, U, V = 0, 1, 2
+    blocks = [
+        Block("IC_eta", [point(0.0), X, Y], [Term(1.0, (0, 0, 0), ETA)], sd * sd, True, eta_obs),
+        Block("IC_u", [point(0.0), X, Y], [Term(1.0, (0, 0, 0), U)], jitter * (hx * hy) ** 2, True, np.zeros(nx * ny)),
+        Block("IC_v", [point(0.0), X, Y], [Term(1.0, (0, 0, 0), V)], jitter * (hx * hy) ** 2, True, np.zeros(nx * ny)),
+    ]
+    c = float(np.sqrt(g * H))
+
+    def rad(face):
+        if face == "BCx0":
+            return [Term(1.0, (1, 0, 0), ETA), Term(-c, (0, 1, 0), ETA)]
+        if face == "BCx1":
+            return [Term(1.0, (1, 0, 0), ETA), Term(c, (0, 1, 0), ETA)]
+        if face == "BCy0":
+            return [Term(1.0, (1, 0, 0), ETA), Term(-c, (0, 0, 1), ETA)]
+        return [Term(1.0, (1, 0, 0), ETA), Term(c, (0, 0, 1), ETA)]
+
+    blocks += _face_blocks(T, X, Y, ht, hx, hy, rad, jitter)
+    n = nt * nx * ny
+    blocks += [
+        Block("PDE_eta", [T, X, Y], [Term(1.0, (1, 0, 0), ETA), Term(H, (0, 1, 0), U), Term(H, (0, 0, 1), V)],
+              0.0, False, np.zeros(n)),
+        Block("PDE_u", [T, X, Y], [Term(1.0, (1, 0, 0), U), Term(g, (0, 1, 0), ETA)], 0.0, False, np.zeros(n)),
+        Block("PDE_v", [T, X, Y], [Term(1.0, (1, 0, 0), V), Term(g, (0, 0, 1), ETA)], 0.0, False, np.zeros(n)),
+    ]
+    kern = [[Kernel1D(q, ell[0]), Kernel1D(q, ell[1]), Kernel1D(q, ell[2])] for _ in range(3)]
+    return Problem(name or f"shallow_water_{nt}x{nx}x{ny}", 3, kern, blocks,
+                   meta=dict(kind="shallow_water", g=g, H=H, c=c))
+
+
+def config4() -> Problem:
+    """BASELINE.json configs[4]: 96 x 192 x 192 cells per output (~10.6M obs)."""
+    return shallow_water_problem(96, 192, 192, name="config4_shallow_water_96x192x192")
+
+
 def cos_ode_problem(n: int, q: int = 2, ell: float = 1.0) -> Problem:
     """PAPER.md Fig. 2 (l.166): du/dx = cos(x) on [0, 2 pi], u(0) = u(2 pi) = 0,
     n FVM cells; the cell observation int_a^b u' = u(b) - u(a) (Eq. 10) with

@@ -1,0 +1,66 @@
+"""BASELINE configs 2-4 (3D wave, advection-diffusion, multi-output shallow
+water) through the C ABI: full-size config-2 matvec against the oracle's
+Kronecker matvec (4-RHS batch, the bench launch configuration), reduced-size
+configs 3/4 against the dense oracle, and full-size properties (symmetry of
+G, linearity) for configs 3/4 where the oracle is too slow."""
+import numpy as np
+import pytest
+
+import gpfvm_inputs as gi
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from oracle.gram import KroneckerGram, dense_gram  # noqa: E402
+from paper_2406_05020_b200 import GpfvmProblem  # noqa: E402
+
+
+def _t(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda:0")
+
+
+def test_config2_fullsize_matvec_4rhs_vs_oracle():
+    p = gi.config2()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    X = gi.random_vectors(p.size, 4, 21)
+    Y = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
+    ref = KroneckerGram(p).matvec(X)
+    assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("builder", [
+    lambda: gi.wave_problem(4, 6, 5),
+    lambda: gi.advdiff_problem(4, 6, 6, n_modes=4),
+    lambda: gi.shallow_water_problem(3, 4, 5),
+])
+def test_reduced_configs_vs_dense_oracle(builder):
+    p = builder()
+    G = dense_gram(p)
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    X = gi.random_vectors(p.size, 3, 4)
+    Y = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
+    ref = X @ G.T
+    assert np.abs(Y - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("cfg", [gi.config3, gi.config4])
+def test_fullsize_3d_properties(cfg):
+    p = cfg()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    X = _t(gi.random_vectors(p.size, 2, 9))
+    Y = gp.gpfvm_gram_matvec(X)
+    # symmetry: x^T G y = y^T G x
+    a = float(torch.dot(X[0], Y[1]))
+    b = float(torch.dot(X[1], Y[0]))
+    assert abs(a - b) <= 1e-10 * (abs(a) + abs(b))
+    # linearity of the batch: G(x0 + 2 x1) = G x0 + 2 G x1
+    Z = gp.gpfvm_gram_matvec((X[0] + 2 * X[1]).reshape(1, -1).contiguous())
+    ref = Y[0] + 2 * Y[1]
+    assert float((Z[0] - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+    # positive semi-definite in the sampled directions
+    assert float(torch.dot(X[0], Y[0])) > 0
