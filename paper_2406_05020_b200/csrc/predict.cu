@@ -63,6 +63,7 @@ unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>
 
 // cross factors between a grid (points, order 0) and every block with a term on `out`
 struct CrossPlan {
+  DevBuf w0, w1;  // KronSum workspaces
   std::vector<Factor> factors;
   std::vector<std::vector<KronTerm>> terms;  // per block J
   int gshape[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
@@ -115,18 +116,33 @@ static void build_cross(gpfvm_problem* p, const gpfvm_grid& g, int row0, int row
   }
 }
 
+// Y_r = beta Y_r + scale * K_{*J} X_r for R vectors through the fused KronSum plan
+static void cross_apply(gpfvm_problem* p, CrossPlan& cp, int J, double scale, const double* X, int64_t ldx, double* Y,
+                        int64_t ldy, int R, double beta, cudaStream_t s) {
+  std::vector<double> coefs;
+  std::vector<std::vector<const double*>> fs;
+  for (const auto& t : cp.terms[J]) {
+    coefs.push_back(scale * t.coef);
+    std::vector<const double*> f;
+    for (int i = 0; i < p->ndim; i++) f.push_back(cp.factors[t.fid[i]].data.ptr);
+    fs.push_back(f);
+  }
+  KronSum ks;
+  ks.build(p->ndim, p->blocks[J].shape, cp.gshape, coefs, fs, s);
+  size_t need = (size_t)std::max<int64_t>(1, ks.workspace_per_rhs() * R);
+  cp.w0.ensure(need);
+  cp.w1.ensure(need);
+  ks.apply(X, ldx, Y, ldy, R, beta, cp.w0.ptr, cp.w1.ptr, s);
+  GPFVM_CUDA(cudaStreamSynchronize(s));  // ks (stacked factors) is freed on return
+}
+
 // out[r] (grid slab) = sum_J K_{*J} X_J[r]  (overwrite), R vectors of stride ldx
 static void apply_cross(gpfvm_problem* p, CrossPlan& cp, const double* X, int64_t ldx, double* out, int64_t ldo, int R,
                         double scale, bool overwrite, cudaStream_t s) {
   bool first = overwrite;
   for (int J = 0; J < (int)p->blocks.size(); J++) {
     if (cp.terms[J].empty()) continue;
-    std::vector<KronTerm> ts = cp.terms[J];
-    for (auto& t : ts) t.coef *= scale;
-    std::vector<const KronTerm*> tp;
-    for (auto& t : ts) tp.push_back(&t);
-    apply_terms(p, cp.factors, tp, p->blocks[J].shape, cp.gshape, X + p->blocks[J].offset, ldx, out, ldo, R, first,
-                s, p->ws);
+    cross_apply(p, cp, J, scale, X + p->blocks[J].offset, ldx, out, ldo, R, first ? 0.0 : 1.0, s);
     first = false;
   }
   if (first) {
@@ -206,23 +222,14 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
     eye.ensure((size_t)nJ * nJ);
     set_identity_kernel2<<<gs((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
     count_launch();
-    std::vector<const KronTerm*> tp;
-    for (auto& t : cp.terms[J]) tp.push_back(&t);
-    if (tp.empty()) {
+    if (cp.terms[J].empty()) {
       for (int r = 0; r < nJ; r++) fill(Z.ptr + (pc.boff[jb] + r) * ng, 0.0, ng, s);
     } else {
-      apply_terms(p, cp.factors, tp, p->blocks[J].shape, cp.gshape, eye.ptr, nJ, Z.ptr + pc.boff[jb] * ng, ng, nJ,
-                  true, s, p->ws);
+      cross_apply(p, cp, J, 1.0, eye.ptr, nJ, Z.ptr + pc.boff[jb] * ng, ng, nJ, 0.0, s);
     }
   }
   // Z -= K_{*P} Y  (rows of Y^T through the P cross terms, negated)
-  {
-    std::vector<KronTerm> ts = cp.terms[pc.P];
-    for (auto& t : ts) t.coef = -t.coef;
-    std::vector<const KronTerm*> tp;
-    for (auto& t : ts) tp.push_back(&t);
-    apply_terms(p, cp.factors, tp, p->blocks[pc.P].shape, cp.gshape, pc.YT.ptr, pc.Np, Z.ptr, ng, nb, false, s, p->ws);
-  }
+  cross_apply(p, cp, pc.P, -1.0, pc.YT.ptr, pc.Np, Z.ptr, ng, nb, 1.0, s);
   // T = S^{-1} Z ; var -= colsum(Z o T)
   Gemm g;
   g.M = nb; g.N = (int)ng; g.K = nb;
@@ -273,7 +280,7 @@ void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, do
   GPFVM_CHECK(d == 2, GPFVM_ERR_UNSUPPORTED, "GPFVM_COV_PRECOND: 2D problems only");
   const int64_t per_row = g.n[1];
   const int64_t nbv = p->pc ? std::max<int64_t>(1, p->pc->nb) : 1;
-  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(1.5e9 / 8 / (2 * nbv * per_row))));
+  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(12e9 / 8 / (4 * nbv * per_row))));
   for (int r0 = 0; r0 < g.n[0]; r0 += rows) {
     int rr = std::min(rows, g.n[0] - r0);
     CrossPlan cp;
