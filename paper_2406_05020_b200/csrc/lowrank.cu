@@ -1,0 +1,146 @@
+// Low-rank couplings of a 2D output block fused into one rank-rk update
+// y = U V (see LowRank in problem.h).
+#include "problem.h"
+
+namespace gpfvm {
+
+namespace {
+unsigned gb(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4096)); }
+
+// fixed[m*P + p] = c * src[m]
+__global__ void set_col_kernel(double* fixed, int P, int p, const double* __restrict__ src, int n, double c) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) fixed[(int64_t)m * P + p] = c * src[m];
+}
+// U[r][m][k0+p] = fixed[m][p]
+__global__ void bcast_cols_kernel(double* U, int R, int n0, int rk, int k0, int P, const double* __restrict__ fixed) {
+  int64_t total = (int64_t)R * n0 * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int p = (int)(i % P);
+    int64_t rm = i / P;
+    int m = (int)(rm % n0);
+    U[rm * rk + k0 + p] = fixed[(int64_t)m * P + p];
+  }
+}
+// U[r][m][k0+p] = T[r][p][m]
+__global__ void scatter_cols_kernel(double* U, const double* __restrict__ T, int R, int n0, int rk, int k0, int P) {
+  int64_t total = (int64_t)R * P * n0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int m = (int)(i % n0);
+    int64_t rp = i / n0;
+    int p = (int)(rp % P);
+    int64_t r = rp / P;
+    U[(r * n0 + m) * rk + k0 + p] = T[i];
+  }
+}
+// V[r][k0+p][n] = fixed[p][n]
+__global__ void bcast_rows_kernel(double* V, int R, int rk, int n1, int k0, int P, const double* __restrict__ fixed) {
+  int64_t total = (int64_t)R * P * n1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int n = (int)(i % n1);
+    int64_t rp = i / n1;
+    int p = (int)(rp % P);
+    int64_t r = rp / P;
+    V[(r * rk + k0 + p) * n1 + n] = fixed[(int64_t)p * n1 + n];
+  }
+}
+__global__ void scaled_copy2(double* dst, const double* __restrict__ src, double c, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = c * src[i];
+}
+}  // namespace
+
+// Mark and build the low-rank parts of every 2D output block.
+void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
+  const int nb = (int)p->blocks.size();
+  pl.lowrank.clear();
+  pl.lowrank.resize(nb);
+  pl.block_off.resize(nb);
+  for (int b = 0; b < nb; b++) pl.block_off[b] = p->blocks[b].offset;
+  if (p->ndim != 2 || getenv("GPFVM_NO_LOWRANK")) return;
+  for (int I = 0; I < nb; I++) {
+    LowRank& lr = pl.lowrank[I];
+    lr.n0 = p->blocks[I].shape[0];
+    lr.n1 = p->blocks[I].shape[1];
+    for (int k : pl.by_out[I]) {
+      PairOp& op = pl.pairs[k];
+      const BlockInt& BJ = p->blocks[op.J];
+      if (op.J == I || !(BJ.shape[0] == 1 || BJ.shape[1] == 1)) continue;
+      LowRank::Part part;
+      part.J = op.J;
+      part.type = (BJ.shape[0] == 1) ? 0 : 1;
+      part.k0 = lr.rk;
+      part.nin = part.type == 0 ? BJ.shape[1] : BJ.shape[0];
+      std::vector<const KronTerm*> ts;
+      for (const auto& t : p->terms)
+        if (t.I == I && t.J == op.J) ts.push_back(&t);
+      part.P = (int)ts.size();
+      if (part.P == 0) continue;
+      const int P = part.P;
+      if (part.type == 0) {
+        part.stk.ensure((size_t)P * lr.n1 * part.nin);
+        part.fixed.ensure((size_t)lr.n0 * P);
+        for (int q = 0; q < P; q++) {
+          const Factor& F0 = p->factors[ts[q]->fid[0]];  // n0 x 1
+          const Factor& F1 = p->factors[ts[q]->fid[1]];  // n1 x n'_1
+          scaled_copy2<<<gb((int64_t)lr.n1 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n1 * part.nin,
+                                                                     F1.data.ptr, 1.0, (int64_t)lr.n1 * part.nin);
+          set_col_kernel<<<gb(lr.n0), 256, 0, s>>>(part.fixed.ptr, P, q, F0.data.ptr, lr.n0, ts[q]->coef);
+          count_launch(2);
+        }
+      } else {
+        part.stk.ensure((size_t)P * lr.n0 * part.nin);
+        part.fixed.ensure((size_t)P * lr.n1);
+        for (int q = 0; q < P; q++) {
+          const Factor& F0 = p->factors[ts[q]->fid[0]];  // n0 x n'_0
+          const Factor& F1 = p->factors[ts[q]->fid[1]];  // n1 x 1
+          scaled_copy2<<<gb((int64_t)lr.n0 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n0 * part.nin,
+                                                                     F0.data.ptr, ts[q]->coef, (int64_t)lr.n0 * part.nin);
+          scaled_copy2<<<gb(lr.n1), 256, 0, s>>>(part.fixed.ptr + (int64_t)q * lr.n1, F1.data.ptr, 1.0, lr.n1);
+          count_launch(2);
+        }
+      }
+      lr.rk += P;
+      op.lowrank = true;
+      lr.parts.push_back(std::move(part));
+    }
+  }
+  check_launch("build_lowrank");
+}
+
+void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn, double beta, const int64_t* block_off,
+                    cudaStream_t s) {
+  for (const Part& part : parts) {
+    const double* xJ = x + block_off[part.J];
+    const int P = part.P;
+    Gemm g;
+    g.M = Rn; g.K = part.nin;
+    g.A = xJ; g.a_rs = ldx; g.a_cs = 1;
+    g.B = part.stk.ptr; g.b_rs = 1; g.b_cs = part.nin;
+    if (part.type == 0) {
+      g.N = P * n1;                                   // V[r][k0+p][:] = F1^p x_J
+      g.C = V.ptr + (int64_t)part.k0 * n1; g.c_rs = (int64_t)rk * n1; g.c_cs = 1;
+      run_gemm(g, s);
+      bcast_cols_kernel<<<gb((int64_t)Rn * n0 * P), 256, 0, s>>>(U.ptr, Rn, n0, rk, part.k0, P, part.fixed.ptr);
+    } else {
+      g.N = P * n0;                                   // T[r][p][:] = c_p F0^p x_J
+      g.C = T.ptr; g.c_rs = (int64_t)P * n0; g.c_cs = 1;
+      run_gemm(g, s);
+      scatter_cols_kernel<<<gb((int64_t)Rn * P * n0), 256, 0, s>>>(U.ptr, T.ptr, Rn, n0, rk, part.k0, P);
+      bcast_rows_kernel<<<gb((int64_t)Rn * P * n1), 256, 0, s>>>(V.ptr, Rn, rk, n1, part.k0, P, part.fixed.ptr);
+      count_launch();
+    }
+    count_launch();
+  }
+  // y_r = beta y_r + U_r V_r   (n0 x rk) (rk x n1)
+  Gemm g;
+  g.M = n0; g.N = n1; g.K = rk;
+  g.A = U.ptr; g.a_rs = rk; g.a_cs = 1; g.a_b1 = (int64_t)n0 * rk;
+  g.B = V.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = (int64_t)rk * n1;
+  g.C = y; g.c_rs = n1; g.c_cs = 1; g.c_b1 = ldy;
+  g.batch1 = Rn;
+  g.beta = beta;
+  run_gemm(g, s);
+  check_launch("LowRank::apply");
+}
+
+}  // namespace gpfvm

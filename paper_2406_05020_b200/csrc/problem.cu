@@ -259,6 +259,7 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
     }
   plan->w0.resize(nb);
   plan->w1.resize(nb);
+  build_lowrank(p, *plan, s);
   p->plan = std::move(plan);
 }
 
@@ -268,8 +269,14 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
   // noise-free block: the first pair overwrites (beta = 0), saving one read-modify-write pass
   bool overwrite = (B.noise == 0.0) && !pl.by_out[I].empty();
   if (!overwrite) vec_scale_add(y + B.offset, x + B.offset, p->noise.ptr + B.offset, B.size, nrhs, ld, s);
+  LowRank& lr = pl.lowrank[I];
+  if (lr.rk > 0) {
+    lr.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), s);
+    overwrite = false;
+  }
   for (int k : pl.by_out[I]) {
     const PairOp& op = pl.pairs[k];
+    if (op.lowrank) continue;
     op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr,
                 pl.w1[I].ptr, s);
     overwrite = false;
@@ -286,6 +293,18 @@ static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
       pl.release_graphs();  // captured graphs reference the old buffers
       pl.w0[I].ensure(n);
       pl.w1[I].ensure(n);
+    }
+    LowRank& lr = pl.lowrank[I];
+    if (lr.rk > 0) {
+      int pmax = 1;
+      for (const auto& part : lr.parts) pmax = std::max(pmax, part.P);
+      size_t nu = (size_t)nrhs * lr.n0 * lr.rk, nv = (size_t)nrhs * lr.rk * lr.n1, nt = (size_t)nrhs * pmax * lr.n0;
+      if (lr.U.n < nu || lr.V.n < nv || lr.T.n < nt) {
+        pl.release_graphs();
+        lr.U.ensure(nu);
+        lr.V.ensure(nv);
+        lr.T.ensure(nt);
+      }
     }
   }
 }

@@ -76,6 +76,27 @@ struct KronSum {
 struct PairOp {
   int I = 0, J = 0;
   KronSum ks;
+  bool lowrank = false;  // folded into the output block's LowRank update
+};
+
+// 2D output block: couplings from blocks with a singleton dimension are
+// rank-P updates  sum_p u_p v_p^T  (u: n0, v: n1) — IC-like blocks (n'_0 = 1):
+// u_p = c_p F0^p[:,0] fixed, v_p = F1^p x_J; BC-like blocks (n'_1 = 1):
+// u_p = c_p F0^p x_J, v_p = F1^p[:,0] fixed.  All of them are evaluated into
+// U (n0 x rk) and V (rk x n1) per vector and applied as ONE batched GEMM
+// y = U V, replacing one read-modify-write pass per coupling.
+struct LowRank {
+  struct Part {
+    int J = 0, type = 0, P = 0, k0 = 0, nin = 0;  // type 0: IC-like, 1: BC-like
+    DevBuf stk;    // type 0: F1^p stacked (P*n1 x n'_1); type 1: c_p F0^p stacked (P*n0 x n'_0)
+    DevBuf fixed;  // type 0: c_p F0^p[:,0] as [n0][P]; type 1: F1^p[:,0] as [P][n1]
+  };
+  int n0 = 0, n1 = 0, rk = 0;
+  std::vector<Part> parts;
+  DevBuf U, V, T;
+  int R = 0;
+  void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, const int64_t* block_off,
+             cudaStream_t s);
 };
 
 // Matvec plan: one KronSum per nonzero block pair, grouped by output block
@@ -83,6 +104,8 @@ struct PairOp {
 struct MatvecPlan {
   std::vector<PairOp> pairs;
   std::vector<std::vector<int>> by_out;
+  std::vector<LowRank> lowrank;  // per output block (rk = 0: unused)
+  std::vector<int64_t> block_off;
   std::vector<DevBuf> w0, w1;  // per output-block branch
   std::vector<cudaStream_t> branch;
   cudaStream_t cap = nullptr;
@@ -135,6 +158,7 @@ void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std
                  bool overwrite, cudaStream_t s, Workspace& ws);
 void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s);
 void build_plan(gpfvm_problem* p, cudaStream_t s);
+void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s);
 double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape);
 int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr);
 
