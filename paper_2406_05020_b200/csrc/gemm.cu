@@ -359,6 +359,7 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
     check_launch("dgemm_generic_kernel");
     return;
   }
+  if (try_cutlass_gemm(g, s)) return;
   const bool brow = (g.b_cs == 1);
   const int64_t b_ld = brow ? g.b_rs : g.b_cs;
   const bool v16 = aligned16(g.A) && aligned16(g.B) && even(g.a_rs) && even(b_ld) && even(g.a_b1) &&

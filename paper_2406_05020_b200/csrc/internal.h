@@ -98,6 +98,7 @@ struct Gemm {
   double alpha = 1.0, beta = 0.0;
 };
 void run_gemm(const Gemm& g, cudaStream_t s);
+bool try_cutlass_gemm(const Gemm& g, cudaStream_t s);  // cutlass_gemm.cu
 double gemm_flops(const Gemm& g);
 
 // ---- small dense linear algebra (linalg.cu) ---------------------------------------

@@ -26,6 +26,21 @@ __global__ void scaled_copy_kernel(double* dst, const double* __restrict__ src, 
 }
 unsigned gsz(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048)); }
 
+// 2D restacking so that both stages are plain GEMMs (no K-segments):
+//   mode 0: dst[(r*P + p)*cols + k] = c * src[r*cols + k]     rows interleaved by term
+//   mode 1: dst[r*(P*cols) + p*cols + k] = c * src[r*cols + k] columns concatenated by term
+//   mode 2: dst[r*(cols*P) + k*P + p] = c * src[r*cols + k]   columns interleaved by term
+__global__ void restack_kernel(double* dst, const double* __restrict__ src, double c, int p, int P, int rows, int cols,
+                               int mode) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i / cols, k = i % cols;
+    int64_t o = (mode == 0) ? (r * P + p) * cols + k : (mode == 1 ? r * ((int64_t)P * cols) + (int64_t)p * cols + k
+                                                                  : r * ((int64_t)cols * P) + k * P + p);
+    dst[o] = c * src[i];
+  }
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -53,6 +68,29 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
   if (P == 0) return;
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
   const int first = rev ? d - 1 : 0;
+  if (d == 2) {
+    // plain-GEMM layouts: forward: stk0 rows interleaved (j0,p) with c_p,
+    // stk1 columns concatenated (p,k); reverse: stk1 blocks (p,j1) with c_p, stk0 columns
+    // interleaved (k,p).
+    for (int i = 0; i < 2; i++) stk[i].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[i] * nin[i] * P));
+    for (int p = 0; p < P; p++) {
+      if (!rev) {
+        restack_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr, factors[p][0], coefs[p], p, P,
+                                                                       nout[0], nin[0], 0);
+        restack_kernel<<<gsz((int64_t)nout[1] * nin[1]), 256, 0, s>>>(stk[1].ptr, factors[p][1], 1.0, p, P, nout[1],
+                                                                       nin[1], 1);
+      } else {
+        scaled_copy_kernel<<<gsz((int64_t)nout[1] * nin[1]), 256, 0, s>>>(stk[1].ptr + (int64_t)p * nout[1] * nin[1],
+                                                                           factors[p][1], coefs[p],
+                                                                           (int64_t)nout[1] * nin[1]);
+        restack_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr, factors[p][0], 1.0, p, P, nout[0],
+                                                                       nin[0], 2);
+      }
+      count_launch(2);
+    }
+    check_launch("KronSum::build (2D)");
+    return;
+  }
   for (int i = 0; i < d; i++) {
     int64_t fs = (int64_t)nout[i] * nin[i];
     stk[i].ensure((size_t)std::max<int64_t>(1, fs * P));
@@ -105,6 +143,38 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     return;
   }
   const int l = d - 1;
+  if (d == 2) {
+    const int64_t z0 = (int64_t)P * (rev ? nin[0] * nout[1] : nout[0] * nin[1]);
+    Gemm g0, g1;
+    if (!rev) {
+      // Z_r[(j0,p)][k1] = sum_k0 c_p F0^p[j0][k0] X_r[k0][k1]
+      g0.M = P * nout[0]; g0.N = nin[1]; g0.K = nin[0];
+      g0.A = stk[0].ptr; g0.a_rs = nin[0]; g0.a_cs = 1;
+      g0.B = x; g0.b_rs = nin[1]; g0.b_cs = 1; g0.b_b1 = ldx;
+      g0.C = w0; g0.c_rs = nin[1]; g0.c_cs = 1; g0.c_b1 = z0;
+      // Y_r[j0][j1] = sum_(p,k1) Z_r[j0][(p,k1)] F1^p[j1][k1]
+      g1.M = nout[0]; g1.N = nout[1]; g1.K = P * nin[1];
+      g1.A = w0; g1.a_rs = (int64_t)P * nin[1]; g1.a_cs = 1; g1.a_b1 = z0;
+      g1.B = stk[1].ptr; g1.b_rs = 1; g1.b_cs = (int64_t)P * nin[1];
+    } else {
+      // Z_r[k0][(p,j1)] = sum_k1 X_r[k0][k1] c_p F1^p[j1][k1]
+      g0.M = nin[0]; g0.N = P * nout[1]; g0.K = nin[1];
+      g0.A = x; g0.a_rs = nin[1]; g0.a_cs = 1; g0.a_b1 = ldx;
+      g0.B = stk[1].ptr; g0.b_rs = 1; g0.b_cs = nin[1];
+      g0.C = w0; g0.c_rs = (int64_t)P * nout[1]; g0.c_cs = 1; g0.c_b1 = z0;
+      // Y_r[j0][j1] = sum_(k0,p) F0^p[j0][k0] Z_r[(k0,p)][j1]
+      g1.M = nout[0]; g1.N = nout[1]; g1.K = nin[0] * P;
+      g1.A = stk[0].ptr; g1.a_rs = (int64_t)nin[0] * P; g1.a_cs = 1;
+      g1.B = w0; g1.b_rs = nout[1]; g1.b_cs = 1; g1.b_b1 = z0;
+    }
+    g0.batch1 = R;
+    g1.C = y; g1.c_rs = nout[1]; g1.c_cs = 1; g1.c_b1 = ldy;
+    g1.batch1 = R;
+    g1.beta = beta;
+    run_gemm(g0, s);
+    run_gemm(g1, s);
+    return;
+  }
   if (!rev) {
     // stage 0: stacked M over p
     int64_t rest = 1;
