@@ -376,7 +376,12 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
 
 using namespace gpfvm;
 
-gpfvm_problem::~gpfvm_problem() { destroy_precond(pc); }
+gpfvm_problem::~gpfvm_problem() {
+  destroy_precond(pc);
+  plan.reset();
+  for (auto st : pipe)
+    if (st) cudaStreamDestroy(st);
+}
 
 extern "C" {
 
@@ -505,6 +510,38 @@ int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, in
     const double* xd = x;
     double* yd = y;
     size_t n = (size_t)ld * (nrhs - 1) + p->N;
+    if (!dx && !dy && nrhs >= 8) {
+      // host -> device -> host pipeline over RHS chunks on three internal
+      // streams: H2D of chunk c+1 and D2H of chunk c-1 overlap the matvec of c
+      GPFVM_CHECK(p->assembled && p->plan, GPFVM_ERR_STATE, "gpfvm_gram_matvec: call gpfvm_assemble_factors first");
+      if (!p->pipe[0])
+        for (int i = 0; i < 3; i++) GPFVM_CUDA(cudaStreamCreateWithFlags(&p->pipe[i], cudaStreamNonBlocking));
+      const int nch = 4, csz = (nrhs + nch - 1) / nch;
+      p->stage_in.ensure(n);
+      p->stage_out.ensure(n);
+      std::vector<cudaEvent_t> evs(2 * nch + 1);
+      for (auto& e : evs) GPFVM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      GPFVM_CUDA(cudaEventRecord(evs[2 * nch], s));  // prior work on the caller's stream (assembly)
+      for (int i = 0; i < 3; i++) GPFVM_CUDA(cudaStreamWaitEvent(p->pipe[i], evs[2 * nch], 0));
+      for (int c = 0; c < nch; c++) {
+        const int r0 = c * csz, rc = std::min(csz, nrhs - r0);
+        if (rc <= 0) break;
+        const size_t off = (size_t)r0 * ld, cnt = (size_t)ld * (rc - 1) + p->N;
+        GPFVM_CUDA(cudaMemcpyAsync(p->stage_in.ptr + off, x + off, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                                   p->pipe[0]));
+        GPFVM_CUDA(cudaEventRecord(evs[c], p->pipe[0]));
+        GPFVM_CUDA(cudaStreamWaitEvent(p->pipe[1], evs[c], 0));
+        matvec_device(p, p->stage_in.ptr + off, p->stage_out.ptr + off, rc, ld, p->pipe[1]);
+        GPFVM_CUDA(cudaEventRecord(evs[nch + c], p->pipe[1]));
+        GPFVM_CUDA(cudaStreamWaitEvent(p->pipe[2], evs[nch + c], 0));
+        GPFVM_CUDA(cudaMemcpyAsync(y + off, p->stage_out.ptr + off, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                                   p->pipe[2]));
+      }
+      GPFVM_CUDA(cudaStreamSynchronize(p->pipe[2]));
+      GPFVM_CUDA(cudaStreamSynchronize(p->pipe[1]));
+      for (auto& e : evs) cudaEventDestroy(e);
+      return;
+    }
     if (!dx) {
       p->stage_in.ensure(n);
       GPFVM_CUDA(cudaMemcpyAsync(p->stage_in.ptr, x, n * sizeof(double), cudaMemcpyHostToDevice, s));

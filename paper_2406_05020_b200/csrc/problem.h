@@ -144,6 +144,7 @@ struct gpfvm_problem {
   gpfvm::DevBuf stage_in, stage_out;  // host-pointer staging
   std::unique_ptr<gpfvm::MatvecPlan> plan;
   gpfvm::DevBuf pcg_s, pcg_z;           // fixed PCG operands (graph-replayable matvec)
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // host-pointer matvec pipeline (H2D, compute, D2H)
   ~gpfvm_problem();
 };
 

@@ -130,6 +130,18 @@ def test_matvec_config1_fullsize_vs_oracle_kronecker():
     _close(Y, ref, 1e-12, elem=False)
 
 
+def test_host_pointer_pipeline_config1():
+    """nrhs >= 8 with host buffers runs the chunked H2D/compute/D2H pipeline;
+    same numbers as the device-pointer path (up to GEMM-kernel choice)."""
+    p = gi.config1()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    X = np.ascontiguousarray(gi.random_vectors(p.size, 16, 3))
+    Yd = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
+    Yh = gp.gpfvm_gram_matvec(X)
+    assert np.abs(Yh - Yd).max() <= 1e-14 * np.abs(Yd).max()
+
+
 def test_solve_and_predict_config0():
     p = gi.config0()
     G = dense_gram(p)
