@@ -162,6 +162,8 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
   GPFVM_CHECK(p->pc && p->pc->type == GPFVM_PRECOND_BLOCK_FD, GPFVM_ERR_STATE,
               "GPFVM_COV_PRECOND needs a preceding gpfvm_solve with the BLOCK_FD preconditioner");
   Precond& pc = *p->pc;
+  GPFVM_CHECK(!pc.blockjacobi, GPFVM_ERR_UNSUPPORTED,
+              "GPFVM_COV_PRECOND needs the exact (2D two-term, block-LDL) preconditioner; use GPFVM_COV_ITERGP");
   const int n0 = pc.n0, n1 = pc.n1;
   const int g0 = cp.gshape[0], g1 = cp.gshape[1];
   // --- FD part -------------------------------------------------------------

@@ -33,8 +33,33 @@ struct KronTerm {
   int fid[GPFVM_MAX_DIMS] = {-1, -1, -1, -1};
 };
 
+// Fused sum of Kronecker products of one block pair (kron.cu, DESIGN.md §4.2)
+struct KronSum {
+  int d = 0, P = 0;
+  bool rev = false;  // contraction order: dim d-1 first (chosen by flop count)
+  int nin[GPFVM_MAX_DIMS] = {1, 1, 1, 1}, nout[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
+  DevBuf stk[GPFVM_MAX_DIMS];  // stacked factors per dim (coefficients folded into dim 0)
+  void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
+             const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
+  int64_t workspace_per_rhs() const;
+  double flops_per_rhs() const;
+  // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
+  void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
+             cudaStream_t s) const;
+};
+
+// Per-block fast-diagonalisation (bjfd.cu)
+struct BlockFD {
+  int J = 0, d = 0;
+  int shape[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
+  DevBuf Q[GPFVM_MAX_DIMS], Qt[GPFVM_MAX_DIMS], Dinv, w0, w1, tmp;
+  KronSum fwd, bwd;
+};
+
 // Block-LDL / fast-diagonalisation preconditioner state (solve.cu)
 struct Precond {
+  bool blockjacobi = false;      // general case: block-Jacobi FD (bj) instead of exact LDL
+  std::vector<BlockFD> bj;
   int type = GPFVM_PRECOND_NONE;
   int P = -1;
   int n0 = 0, n1 = 0;
@@ -56,21 +81,6 @@ struct Krylov {   // kept IterGP actions
 
 struct Workspace {
   DevBuf t0, t1;
-};
-
-// Fused sum of Kronecker products of one block pair (kron.cu, DESIGN.md §4.2)
-struct KronSum {
-  int d = 0, P = 0;
-  bool rev = false;  // contraction order: dim d-1 first (chosen by flop count)
-  int nin[GPFVM_MAX_DIMS] = {1, 1, 1, 1}, nout[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
-  DevBuf stk[GPFVM_MAX_DIMS];  // stacked factors per dim (coefficients folded into dim 0)
-  void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
-             const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
-  int64_t workspace_per_rhs() const;
-  double flops_per_rhs() const;
-  // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
-  void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-             cudaStream_t s) const;
 };
 
 struct PairOp {
@@ -171,5 +181,7 @@ void solve_impl(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
 void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var,
                   int cov_mode, cudaStream_t s);
 void destroy_precond(Precond* pc);
+void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s);
+void apply_block_fd(const BlockFD& bf, const double* r, double* z, int64_t n, cudaStream_t s);
 
 }  // namespace gpfvm

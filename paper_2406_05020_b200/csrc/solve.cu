@@ -316,20 +316,33 @@ static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
   auto pc = new Precond();
   try {
     pc->type = type;
-    int ndefl = 0;
+    int ndefl = 0, nfree = 0;
+    int64_t nb = 0;
     for (int b = 0; b < (int)p->blocks.size(); b++) {
       if (!p->blocks[b].deflate) {
-        GPFVM_CHECK(pc->P < 0, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: exactly one non-deflated block supported");
         pc->P = b;
+        nfree++;
       } else {
         ndefl++;
+        nb += p->blocks[b].size;
       }
     }
-    GPFVM_CHECK(pc->P >= 0, GPFVM_ERR_UNSUPPORTED, "BLOCK_FD: no non-deflated (PDE) block");
+    // exact path: one 2D two-term PDE block + a dense IC/BC Schur
+    // complement; otherwise block-Jacobi fast diagonalisation (§5.4)
+    const bool exact = nfree == 1 && p->ndim == 2 && p->blocks[pc->P].terms.size() == 2 &&
+                       p->blocks[pc->P].terms[0].output == p->blocks[pc->P].terms[1].output && nb <= 16384 &&
+                       getenv("GPFVM_FORCE_BJFD") == nullptr;
     PhaseTimer pt(s);
-    build_fd(p, *pc, s);
-    pt.mark("fd: 2 x sygv");
-    build_ldl(p, *pc, s);
+    if (exact) {
+      build_fd(p, *pc, s);
+      pt.mark("fd: 2 x sygv");
+      build_ldl(p, *pc, s);
+    } else {
+      pc->blockjacobi = true;
+      pc->bj.resize(p->blocks.size());
+      for (int b = 0; b < (int)p->blocks.size(); b++) build_block_fd(p, b, pc->bj[b], s);
+      pt.mark("block-Jacobi FD");
+    }
   } catch (...) {
     delete pc;
     throw;
@@ -341,6 +354,13 @@ static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
 // z = P^{-1} r (single vector, z != r)
 void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s) {
   Precond& pc = *p->pc;
+  if (pc.blockjacobi) {
+    for (const auto& bf : pc.bj) {
+      const BlockInt& B = p->blocks[bf.J];
+      apply_block_fd(bf, r + B.offset, z + B.offset, B.size, s);
+    }
+    return;
+  }
   const BlockInt& BP = p->blocks[pc.P];
   const double* rp = r + BP.offset;
   double* zp = z + BP.offset;
