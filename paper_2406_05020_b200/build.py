@@ -16,7 +16,7 @@ def cutlass_include():
     return None
 
 
-SOURCES = ["assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "cutlass_gemm.cu"]
+SOURCES = ["pool.cu", "assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "cutlass_gemm.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",
          "-Xcompiler", "-fPIC"]
 

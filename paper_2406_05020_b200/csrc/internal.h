@@ -37,6 +37,16 @@ inline void count_launch(int64_t n = 1) { g_launches.fetch_add(n, std::memory_or
 void check_launch(const char* what);
 
 // ---- device buffer -------------------------------------------------------------
+// Device allocations go through a size-bucketed caching pool: releasing a
+// buffer returns it to the pool instead of calling cudaFree (which would
+// synchronise the whole device and serialise concurrent streams).  A pooled
+// block is handed out again only to a later allocation; temporaries are
+// released after the stream that used them has been synchronised or when the
+// next user is on the same stream (stream order), as everywhere in this library.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p, size_t bytes);
+void pool_trim();  // cudaFree every cached block of the current device
+
 struct DevBuf {
   double* ptr = nullptr;
   size_t n = 0;
@@ -50,7 +60,7 @@ struct DevBuf {
   }
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) pool_free(ptr, n * sizeof(double));
     ptr = nullptr;
     n = 0;
   }
@@ -58,7 +68,7 @@ struct DevBuf {
     if (count <= n) return;
     release();
     if (count == 0) return;
-    GPFVM_CUDA(cudaMalloc(&ptr, count * sizeof(double)));
+    ptr = static_cast<double*>(pool_alloc(count * sizeof(double)));
     n = count;
   }
 };

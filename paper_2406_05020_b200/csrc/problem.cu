@@ -447,6 +447,7 @@ int gpfvm_problem_destroy(gpfvm_problem* p) {
     if (!p) return;
     cudaSetDevice(p->device);
     delete p;
+    pool_trim();
   });
 }
 

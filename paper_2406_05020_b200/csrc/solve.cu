@@ -15,6 +15,7 @@
 //   s = P^{-1} r ; z = G s ; c_j = d_j.z / eta_j ; d = s - sum c_j d_j ;
 //   Gd = z - sum c_j Gd_j ; eta = z.d ; a = d.r / eta ; x += a d ; r -= a Gd
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -171,8 +172,35 @@ static void build_fd(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   pc.Vt.ensure((size_t)n0 * n0);
   pc.W.ensure((size_t)n1 * n1);
   pc.Dinv.ensure((size_t)n0 * n1);
-  sygv(p->factors[fB0].data.ptr, p->factors[fA0].data.ptr, n0, pc.V.ptr, lam.ptr, s);
-  sygv(p->factors[fA1].data.ptr, p->factors[fB1].data.ptr, n1, pc.W.ptr, mu.ptr, s);
+  // the two generalised eigenproblems are independent and each keeps only
+  // n/32 CTAs busy per Jacobi round: run them concurrently (two host threads,
+  // two streams; sygv synchronises its own stream)
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+  {
+    cudaStream_t s2[2];
+    for (auto& st : s2) GPFVM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev = 0;
+    GPFVM_CUDA(cudaGetDevice(&dev));
+    Error err{GPFVM_OK, ""};
+    std::thread th([&] {
+      try {
+        cudaSetDevice(dev);
+        sygv(p->factors[fA1].data.ptr, p->factors[fB1].data.ptr, n1, pc.W.ptr, mu.ptr, s2[1]);
+      } catch (const Error& e) {
+        err = e;
+      }
+    });
+    try {
+      sygv(p->factors[fB0].data.ptr, p->factors[fA0].data.ptr, n0, pc.V.ptr, lam.ptr, s2[0]);
+    } catch (...) {
+      th.join();
+      for (auto st : s2) cudaStreamDestroy(st);
+      throw;
+    }
+    th.join();
+    for (auto st : s2) cudaStreamDestroy(st);
+    if (err.code != GPFVM_OK) throw err;
+  }
   transpose(pc.V.ptr, pc.Vt.ptr, n0, n0, s);
   colsumsq_kernel<<<g1(n0, 128), 128, 0, s>>>(pc.V.ptr, n0, vv.ptr);
   colsumsq_kernel<<<g1(n1, 128), 128, 0, s>>>(pc.W.ptr, n1, ww.ptr);
