@@ -151,7 +151,7 @@ __global__ void eye_kernel(double* A, int n) {
 // ---- block one-sided Jacobi ----------------------------------------------------
 constexpr int JB = 16;          // columns per block
 constexpr int JC = 2 * JB;      // columns per CTA (pair of blocks)
-constexpr int JT = 512;         // threads per CTA
+constexpr int JT = 256;         // threads per CTA (<= 255 registers: no spills in the X.Q update)
 __constant__ int c_inner_sweeps = 1;
 
 // Xc, Vc: column-major n x n (column j at Xc + j*n).  pairs: (blk_a, blk_b) per CTA.
@@ -290,20 +290,34 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
     }
   }
   __syncthreads();
-  // X <- X Q (rows in parallel), write back; then V <- V Q
-  for (int r = t; r < n; r += JT) {
-    double xr[JC];
-    for (int c = 0; c < cnt; c++) xr[c] = Xs[(size_t)c * n + r];
-    for (int j = 0; j < cnt; j++) {
-      double s = 0.0;
-      for (int c = 0; c < cnt; c++) s = fma(xr[c], Q[c * (JC + 1) + j], s);
-      Xc[(size_t)col_of[j] * n + r] = s;
+  // X <- X Q, then V <- V Q (V staged through the same shared buffer).  Rows
+  // in parallel; per row JC independent register accumulators (fully unrolled,
+  // no local-memory arrays), operands from shared memory (X column-major:
+  // consecutive rows -> consecutive banks; Q broadcast).  Unused columns
+  // (cnt < JC) carry zeros in Q.
+  for (int pass = 0; pass < 2; pass++) {
+    double* dst = pass == 0 ? Xc : Vc;
+    if (pass == 1) {
+      __syncthreads();
+      for (int i = t; i < cnt * n; i += JT) {
+        int c = i / n, r = i % n;
+        Xs[(size_t)c * n + r] = Vc[(size_t)col_of[c] * n + r];
+      }
+      __syncthreads();
     }
-    for (int c = 0; c < cnt; c++) xr[c] = Vc[(size_t)col_of[c] * n + r];
-    for (int j = 0; j < cnt; j++) {
-      double s = 0.0;
-      for (int c = 0; c < cnt; c++) s = fma(xr[c], Q[c * (JC + 1) + j], s);
-      Vc[(size_t)col_of[j] * n + r] = s;
+    for (int r = t; r < n; r += JT) {
+      double acc[JC];
+#pragma unroll
+      for (int j = 0; j < JC; j++) acc[j] = 0.0;
+#pragma unroll
+      for (int c = 0; c < JC; c++) {
+        const double xv = (c < cnt) ? Xs[(size_t)c * n + r] : 0.0;
+#pragma unroll
+        for (int j = 0; j < JC; j++) acc[j] = fma(xv, Q[c * (JC + 1) + j], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < JC; j++)
+        if (j < cnt) dst[(size_t)col_of[j] * n + r] = acc[j];
     }
   }
 }
