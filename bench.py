@@ -142,6 +142,7 @@ def main():
     ap.add_argument("--nrhs", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -263,6 +264,38 @@ def main():
                 "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
                 "traffic": None, "flops_per_launch": flops_mv}
 
+    sharded = None
+    if world > 1 and not args.no_sharded:
+        # time-sharded PDE-block operator of BASELINE config 3 (8.4M obs): NCCL all-to-all
+        # re-partition + one K-concatenated time GEMM per matvec
+        try:
+            from paper_2406_05020_b200.dist import GpuOps, ShardedKron, block_kron_terms
+            p3 = gi.config3()
+            P3 = len(p3.blocks) - 1
+            ops = GpuOps(dev)
+            coefs, facs = block_kron_terms(p3, P3, local)
+            shape = p3.blocks[P3].shape
+            A = ShardedKron(ops, shape, coefs, facs, None, rank, world)
+            nloc = (shape[0] // world) * shape[1] * shape[2]
+            xs = torch.randn(nloc, dtype=torch.float64, device=dev)
+            for _ in range(2):
+                A.matvec(xs)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = ev(), ev()
+            e0.record()
+            for _ in range(5):
+                A.matvec(xs)
+            e1.record()
+            torch.cuda.synchronize()
+            tt = torch.tensor([e0.elapsed_time(e1) / 5], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            npde = shape[0] * shape[1] * shape[2]
+            sharded = {"workload": "config3 PDE block (time-sharded)", "n_obs": int(npde), "ms": float(tt.item()),
+                       "GB_s": npde * 16 / (tt.item() * 1e-3) / 1e9, "terms": len(coefs),
+                       "comm_bytes_per_matvec": (len(coefs) + 1) * npde * 8}
+        except Exception as e:  # never break the headline line
+            sharded = {"error": repr(e)[:200]}
     if rank == 0:
         cb = None
         if not args.no_cpu_baseline and world == 1:
@@ -279,7 +312,7 @@ def main():
             "cg_true_rel_residual": rep["true_rel_residual"],
             "ms": {k: float(np.mean(v)) for k, v in times.items()},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
-            "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"),
+            "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"), "sharded": sharded,
         }
         print(json.dumps(line))
     if world > 1:

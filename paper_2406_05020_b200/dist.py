@@ -274,3 +274,33 @@ def sharded_pcg(ops, A: ShardedKron, y_local, precond=None, rtol=1e-8, max_iter=
         norms.append(nr / ny)
     converged = converged or nr <= rtol * ny
     return PCGResult(x, k, nr / ny if ny else 0.0, converged, norms)
+
+
+def block_kron_terms(problem, J, device=0):
+    """Kronecker terms (coefficients, full 1D factors on the GPU) of the diagonal
+    Gram block (J, J), with the exact R6 cancellation of term pairs (the same
+    rule the library applies internally), factors from gpfvm_factor_matrix."""
+    from .api import factor_matrix
+    blk = problem.blocks[J]
+    d = problem.ndim
+    coefs, facs = [], []
+    cache = {}
+    for a, t1 in enumerate(blk.terms):
+        for b, t2 in enumerate(blk.terms):
+            if t1.output != t2.output or b < a:
+                continue
+            c = t1.coeff * t2.coeff
+            if a != b:
+                if sum(t1.order[i] + t2.order[i] for i in range(d)) % 2:
+                    continue
+                c *= 2.0
+            fs = []
+            for i in range(d):
+                key = (t1.output, i, t1.order[i], t2.order[i])
+                if key not in cache:
+                    k = problem.kernels[t1.output][i]
+                    cache[key] = factor_matrix(k, blk.sites[i], t1.order[i], blk.sites[i], t2.order[i], device)
+                fs.append(cache[key])
+            coefs.append(c)
+            facs.append(fs)
+    return coefs, facs

@@ -41,3 +41,23 @@ def test_gpu_sharded_heat_operator_and_pcg(nt, nx):
     a = res.x.cpu().numpy()
     r = KroneckerGram(pde).matvec(a) - b
     assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b)
+
+
+def test_gpu_sharded_3d_pde_block_matches_library():
+    """block_kron_terms (R6 cancellation rebuilt on the host) + ShardedKron on a
+    3D advection-diffusion PDE block == the library's own Gram matvec restricted
+    to that block (the bench's N>1 sharded measurement path, world size 1)."""
+    from paper_2406_05020_b200 import GpfvmProblem
+    from paper_2406_05020_b200.dist import ShardedKron, block_kron_terms
+    p = gi.advdiff_problem(16, 24, 24, n_modes=4)
+    P = len(p.blocks) - 1
+    pde = Problem("pde", 3, p.kernels, [p.blocks[P]])
+    ops = GpuOps("cuda:0")
+    coefs, facs = block_kron_terms(pde, 0)
+    A = ShardedKron(ops, pde.blocks[0].shape, coefs, facs)
+    gp = GpfvmProblem(pde)
+    gp.gpfvm_assemble_factors()
+    x = torch.tensor(gi.random_vectors(pde.size, 1, 4)[0], device="cuda:0")
+    y = A.matvec(x)
+    ref = gp.gpfvm_gram_matvec(x.reshape(1, -1).contiguous())[0]
+    assert float((y - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
