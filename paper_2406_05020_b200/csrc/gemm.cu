@@ -352,7 +352,9 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
     }
     const int threads = g.N >= 128 ? 128 : 32;
     unsigned bx = (unsigned)((g.N + threads - 1) / threads);
-    unsigned by = (unsigned)std::min(g.M, 16);  // each thread loops over several rows
+    // enough blocks to fill the machine; each thread loops over M / by rows
+    const int64_t nbz = std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
+    unsigned by = (unsigned)std::min<int64_t>(g.M, std::max<int64_t>(16, 4096 / std::max<int64_t>(1, (int64_t)bx * nbz)));
     unsigned bz = (unsigned)std::min<int64_t>((int64_t)g.batch1 * g.batch2 * g.batch3, 65535);
     dgemm_generic_kernel<<<dim3(bx, by, bz), threads, 0, s>>>(g);
     count_launch();

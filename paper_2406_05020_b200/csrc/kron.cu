@@ -91,6 +91,22 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
     check_launch("KronSum::build (2D)");
     return;
   }
+  if (d == 3 && !rev) {
+    // 3D forward plain layout: stk0 rows interleaved (j0,p) with c_p, stk1 P plain blocks,
+    // stk2 columns concatenated (p,k2)
+    for (int i = 0; i < 3; i++) stk[i].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[i] * nin[i] * P));
+    for (int p = 0; p < P; p++) {
+      restack_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr, factors[p][0], coefs[p], p, P,
+                                                                     nout[0], nin[0], 0);
+      scaled_copy_kernel<<<gsz((int64_t)nout[1] * nin[1]), 256, 0, s>>>(stk[1].ptr + (int64_t)p * nout[1] * nin[1],
+                                                                         factors[p][1], 1.0, (int64_t)nout[1] * nin[1]);
+      restack_kernel<<<gsz((int64_t)nout[2] * nin[2]), 256, 0, s>>>(stk[2].ptr, factors[p][2], 1.0, p, P, nout[2],
+                                                                     nin[2], 1);
+      count_launch(3);
+    }
+    check_launch("KronSum::build (3D)");
+    return;
+  }
   for (int i = 0; i < d; i++) {
     int64_t fs = (int64_t)nout[i] * nin[i];
     stk[i].ensure((size_t)std::max<int64_t>(1, fs * P));
@@ -173,6 +189,50 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     g1.beta = beta;
     run_gemm(g0, s);
     run_gemm(g1, s);
+    return;
+  }
+  if (d == 3 && !rev) {
+    const int64_t n0 = nout[0], n1 = nout[1], n2 = nout[2], m0 = nin[0], m1 = nin[1], m2 = nin[2];
+    const int64_t z0 = (int64_t)P * n0 * m1 * m2;  // [r][(j0,p)][k1][k2]
+    const int64_t z1 = n0 * n1 * P * m2;           // [r][j0][j1][p][k2]
+    Gemm g0, g1, g2;
+    // stage 0: Z0_r[(j0,p)][(k1,k2)] = sum_k0 c_p F0^p[j0][k0] X_r[k0][(k1,k2)]
+    g0.M = (int)(P * n0); g0.N = (int)(m1 * m2); g0.K = (int)m0;
+    g0.A = stk[0].ptr; g0.a_rs = m0; g0.a_cs = 1;
+    g0.B = x; g0.b_rs = m1 * m2; g0.b_cs = 1; g0.b_b1 = ldx;
+    g0.C = w0; g0.c_rs = m1 * m2; g0.c_cs = 1; g0.c_b1 = z0;
+    g0.batch1 = R;
+    run_gemm(g0, s);
+    // stage 1 per (j0, p, r): Z1[j1][k2] = F1^p[j1][:] Z0[j0][p][:][k2], written as [j0][j1][p][k2]
+    g1.M = (int)n1; g1.N = (int)m2; g1.K = (int)m1;
+    g1.A = stk[1].ptr; g1.a_rs = m1; g1.a_cs = 1; g1.a_b2 = n1 * m1;
+    g1.B = w0; g1.b_rs = m2; g1.b_cs = 1;
+    g1.b_b1 = (int64_t)P * m1 * m2; g1.b_b2 = m1 * m2; g1.b_b3 = z0;
+    g1.C = w1; g1.c_rs = (int64_t)P * m2; g1.c_cs = 1;
+    g1.c_b1 = n1 * P * m2; g1.c_b2 = m2; g1.c_b3 = z1;
+    g1.batch1 = (int)n0; g1.batch2 = P; g1.batch3 = R;
+    if (P > 1 && n1 >= 64 && m2 >= 32) {
+      // one plain batched GEMM per term over the combined (r, j0) batch (uniform
+      // strides) so the tensor-op template applies
+      for (int p = 0; p < P; p++) {
+        Gemm gp = g1;
+        gp.A = stk[1].ptr + (int64_t)p * n1 * m1; gp.a_b2 = 0;
+        gp.B = w0 + (int64_t)p * m1 * m2; gp.b_b1 = (int64_t)P * m1 * m2; gp.b_b2 = gp.b_b3 = 0;
+        gp.C = w1 + (int64_t)p * m2; gp.c_b1 = n1 * P * m2; gp.c_b2 = gp.c_b3 = 0;
+        gp.batch1 = (int)(n0 * R); gp.batch2 = gp.batch3 = 1;
+        run_gemm(gp, s);
+      }
+    } else {
+      run_gemm(g1, s);
+    }
+    // stage 2: Y_r[(j0,j1)][j2] = sum_(p,k2) Z1_r[(j0,j1)][(p,k2)] F2^p[j2][k2]
+    g2.M = (int)(n0 * n1); g2.N = (int)n2; g2.K = (int)(P * m2);
+    g2.A = w1; g2.a_rs = (int64_t)P * m2; g2.a_cs = 1; g2.a_b1 = z1;
+    g2.B = stk[2].ptr; g2.b_rs = 1; g2.b_cs = (int64_t)P * m2;
+    g2.C = y; g2.c_rs = n2; g2.c_cs = 1; g2.c_b1 = ldy;
+    g2.batch1 = R;
+    g2.beta = beta;
+    run_gemm(g2, s);
     return;
   }
   if (!rev) {
