@@ -199,6 +199,8 @@ typedef struct {
   double rtol;        /* default 1e-8 */
   int max_iter;       /* default 1000 */
   int precond;        /* GPFVM_PRECOND_* (default BLOCK_FD) */
+  int reorth_window;  /* 0: full reorthogonalisation against every kept direction (default);
+                         w > 0: only the last w (w = 1 is the PCG recurrence) */
 } gpfvm_solve_opts;
 
 typedef struct {

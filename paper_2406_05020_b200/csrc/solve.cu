@@ -478,15 +478,19 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
     copy(d, p->pcg_s.ptr, N, s);
     copy(gd, p->pcg_z.ptr, N, s);
     if (K.k > 0) {
-      // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j
-      dot_many(K.d.ptr, N, gd, N, K.k, dsc, s);
-      coef.resize(K.k);
-      GPFVM_CUDA(cudaMemcpyAsync(coef.data(), dsc, sizeof(double) * K.k, cudaMemcpyDeviceToHost, s));
+      // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j over the last
+      // `w` kept directions (w = k: full reorthogonalisation, §6 l.475; w = 1: the
+      // PCG recurrence, equivalent in exact arithmetic)
+      const int w = (o.reorth_window > 0) ? std::min(o.reorth_window, K.k) : K.k;
+      const int j0 = K.k - w;
+      dot_many(K.d.ptr + (int64_t)j0 * N, N, gd, N, w, dsc, s);
+      coef.resize(w);
+      GPFVM_CUDA(cudaMemcpyAsync(coef.data(), dsc, sizeof(double) * w, cudaMemcpyDeviceToHost, s));
       GPFVM_CUDA(cudaStreamSynchronize(s));
-      for (int j = 0; j < K.k; j++) coef[j] /= K.eta[j];
-      GPFVM_CUDA(cudaMemcpyAsync(dsc, coef.data(), sizeof(double) * K.k, cudaMemcpyHostToDevice, s));
-      axpy_many(d, K.d.ptr, N, dsc, -1.0, N, K.k, s);
-      axpy_many(gd, K.gd.ptr, N, dsc, -1.0, N, K.k, s);
+      for (int j = 0; j < w; j++) coef[j] /= K.eta[j0 + j];
+      GPFVM_CUDA(cudaMemcpyAsync(dsc, coef.data(), sizeof(double) * w, cudaMemcpyHostToDevice, s));
+      axpy_many(d, K.d.ptr + (int64_t)j0 * N, N, dsc, -1.0, N, w, s);
+      axpy_many(gd, K.gd.ptr + (int64_t)j0 * N, N, dsc, -1.0, N, w, s);
     }
     // eta = Gd . d ; a = d . r / eta
     dot_many(d, N, gd, N, 1, dsc, s);

@@ -92,3 +92,22 @@ def test_3d_solve_blockjacobi_fd_vs_cholesky(builder):
     assert np.abs(mean - m_ref).max() <= 1e-6 * max(1e-12, np.abs(m_ref).max())
     v = var.cpu().numpy()
     assert np.all(v >= v_ref - 1e-8) and np.all(v <= 1.0 + 1e-12)
+
+
+@pytest.mark.parametrize("window", [1, 8])
+def test_3d_solve_reorth_window(window):
+    """gpfvm_solve_opts.reorth_window (R7): windowed
+    reorthogonalisation still converges to the Cholesky solution (w = 1 is the
+    plain PCG recurrence, identical to full reorthogonalisation in exact
+    arithmetic)."""
+    p = gi.wave_problem(4, 6, 6)
+    G = dense_gram(p)
+    y = p.rhs()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    alpha, rep = gp.gpfvm_solve(_t(y), rtol=1e-10, max_iter=4000, reorth_window=window)
+    assert rep["converged"], rep
+    a = alpha.cpu().numpy()
+    assert np.linalg.norm(G @ a - y) <= 1e-9 * np.linalg.norm(y)
+    a_ref = np.linalg.solve(G, y)
+    assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
