@@ -6,6 +6,8 @@
 //     (Gram -> in-smem parallel cyclic Jacobi -> rotate columns), tournament
 //     ordering across CTAs; converged columns X = C V = V diag(lambda).
 //   * generalised symmetric-definite eigenproblem via Cholesky reduction.
+#include <mutex>
+#include <thread>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -142,6 +144,12 @@ __global__ void zero_upper_kernel(double* A, int n) {
   if ((idx % n) > (idx / n)) A[idx] = 0.0;
 }
 
+__global__ void scale_scalar_kernel(double* x, double a) { *x *= a; }
+void scale_scalar(double* x, double a, cudaStream_t s) {
+  scale_scalar_kernel<<<1, 1, 0, s>>>(x, a);
+  count_launch();
+}
+
 __global__ void eye_kernel(double* A, int n) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -149,21 +157,59 @@ __global__ void eye_kernel(double* A, int n) {
 }
 
 // ---- block one-sided Jacobi ----------------------------------------------------
-constexpr int JB = 16;          // columns per block
-constexpr int JC = 2 * JB;      // columns per CTA (pair of blocks)
 constexpr int JT = 256;         // threads per CTA (<= 255 registers: no spills in the X.Q update)
 __constant__ int c_inner_sweeps = 1;
 
+// Copy `cnt` columns (ids col_of) of a column-major n-row matrix into shared
+// memory, 4 independent 16-byte loads in flight per thread (n even) so the
+// copy is bandwidth- rather than latency-bound.
+__device__ __forceinline__ void load_cols(double* __restrict__ Xs, const double* __restrict__ G, int n, int cnt,
+                                          const int* col_of) {
+  const int t = threadIdx.x;
+  if ((n & 1) == 0) {
+    const int h = n >> 1, total = cnt * h;
+    for (int base = t; base < total; base += 4 * JT) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        int i = base + u * JT;
+        if (i < total) {
+          int c = i / h, r2 = i - c * h;
+          v[u] = __ldg(reinterpret_cast<const double2*>(G + (size_t)col_of[c] * n) + r2);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        int i = base + u * JT;
+        if (i < total) {
+          int c = i / h, r2 = i - c * h;
+          reinterpret_cast<double2*>(Xs + (size_t)c * n)[r2] = v[u];
+        }
+      }
+    }
+  } else {
+    for (int i = t; i < cnt * n; i += JT) {
+      int c = i / n, r = i % n;
+      Xs[(size_t)c * n + r] = G[(size_t)col_of[c] * n + r];
+    }
+  }
+}
+
 // Xc, Vc: column-major n x n (column j at Xc + j*n).  pairs: (blk_a, blk_b) per CTA.
+template <int JB>
 __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc, int n, int nblk,
                                                           const int* __restrict__ pairs,
-                                                          unsigned long long* offmax) {
+                                                          unsigned long long* offmax,
+                                                          const double* __restrict__ floor_ptr, double skip_tol) {
+  constexpr int JC = 2 * JB;      // columns per CTA (pair of blocks)
   extern __shared__ double sm[];
   double* Xs = sm;                  // [JC][n] column-major (column c at Xs + c*n)
   double* H = Xs + (size_t)JC * n;  // [JC][JC+1]
   double* Q = H + JC * (JC + 1);    // [JC][JC+1]
   __shared__ double cs[JC / 2], sn[JC / 2];
   __shared__ int col_of[JC];
+  __shared__ int pair_ab[JC / 2][2];
+  __shared__ unsigned char ent_a[JC * (JC + 1) / 2], ent_b[JC * (JC + 1) / 2];
   __shared__ int cnt_s;
   const int t = threadIdx.x;
   const int pa = pairs[2 * blockIdx.x], pb = pairs[2 * blockIdx.x + 1];
@@ -175,29 +221,35 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
       for (int j = j0; j < j1; j++) col_of[c++] = j;
     }
     cnt_s = c;
+    int e = 0;
+    for (int a = 0; a < c; a++)
+      for (int b = a; b < c; b++) { ent_a[e] = (unsigned char)a; ent_b[e] = (unsigned char)b; e++; }
   }
   __syncthreads();
   const int cnt = cnt_s;
   if (cnt < 2) return;
-  // load columns
-  for (int i = t; i < cnt * n; i += JT) {
-    int c = i / n, r = i % n;
-    Xs[(size_t)c * n + r] = Xc[(size_t)col_of[c] * n + r];
-  }
+  load_cols(Xs, Xc, n, cnt, col_of);
   __syncthreads();
   // Gram H = Xs^T Xs: one warp per (a, b) entry, lanes stride the rows
-  // (consecutive lanes -> consecutive banks), shuffle reduction.
+  // (consecutive lanes -> consecutive banks), 4 independent partial sums,
+  // shuffle reduction.
   {
     const int warp = t >> 5, lane = t & 31, nw = JT / 32;
     const int npair = cnt * (cnt + 1) / 2;
     for (int e = warp; e < npair; e += nw) {
-      int a = 0, rem = e;
-      while (rem >= cnt - a) { rem -= cnt - a; a++; }
-      int b = a + rem;
+      const int a = ent_a[e], b = ent_b[e];
       const double* xa = Xs + (size_t)a * n;
       const double* xb = Xs + (size_t)b * n;
-      double s = 0.0;
-      for (int r = lane; r < n; r += 32) s = fma(xa[r], xb[r], s);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int r = lane;
+      for (; r + 96 < n; r += 128) {
+        s0 = fma(xa[r], xb[r], s0);
+        s1 = fma(xa[r + 32], xb[r + 32], s1);
+        s2 = fma(xa[r + 64], xb[r + 64], s2);
+        s3 = fma(xa[r + 96], xb[r + 96], s3);
+      }
+      for (; r < n; r += 32) s0 = fma(xa[r], xb[r], s0);
+      double s = (s0 + s1) + (s2 + s3);
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {
         H[a * (JC + 1) + b] = s;
@@ -208,20 +260,30 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
   for (int i = t; i < JC * (JC + 1); i += JT) Q[i] = 0.0;
   __syncthreads();
   for (int i = t; i < cnt; i += JT) Q[i * (JC + 1) + i] = 1.0;
-  // convergence measure (only pairs across the two blocks + within: all)
+  // Convergence measure over all column pairs held by this CTA:
+  // |h_ab| / max(sqrt(h_aa h_bb), floor).  floor = tau ||X||_F^2 (0: the
+  // classical relative measure) treats pairs of columns that are both below
+  // the rounding level of the pencil as converged.  A CTA whose pairs are all
+  // below skip_tol leaves its columns untouched.
+  const double flo = floor_ptr ? *floor_ptr : 0.0;
+  __shared__ double mcta;
   if (t < 32) {
     double m = 0.0;
     for (int i = t; i < cnt * cnt; i += 32) {
       int a = i / cnt, b = i % cnt;
       if (b <= a) continue;
-      double d = sqrt(fabs(H[a * (JC + 1) + a]) * fabs(H[b * (JC + 1) + b]));
+      double d = fmax(sqrt(fabs(H[a * (JC + 1) + a]) * fabs(H[b * (JC + 1) + b])), flo);
       double v = (d > 0.0) ? fabs(H[a * (JC + 1) + b]) / d : 0.0;
       m = fmax(m, v);
     }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (t == 0) atomicMax(offmax, (unsigned long long)__double_as_longlong(m));
+    if (t == 0) {
+      atomicMax(offmax, (unsigned long long)__double_as_longlong(m));
+      mcta = m;
+    }
   }
   __syncthreads();
+  if (mcta < skip_tol) return;
   // parallel cyclic two-sided Jacobi on H (cnt x cnt), round-robin pairing
   const int m = (cnt + 1) & ~1;  // even player count (a dummy if cnt odd)
   const int inner_sweeps = c_inner_sweeps;
@@ -238,7 +300,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
         double c = 1.0, s = 0.0;
         if (q < cnt) {
           double hpp = H[p * (JC + 1) + p], hqq = H[q * (JC + 1) + q], hpq = H[p * (JC + 1) + q];
-          if (fabs(hpq) > 1e-300 && fabs(hpq) > 1e-16 * sqrt(fabs(hpp * hqq))) {
+          if (fabs(hpq) > 1e-300 && fabs(hpq) > 1e-16 * sqrt(fabs(hpp * hqq)) && fabs(hpq) > 1e-16 * flo) {
             double zeta = (hqq - hpp) / (2.0 * hpq);
             double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             c = 1.0 / sqrt(1.0 + tt * tt);
@@ -248,14 +310,14 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
         }
         cs[t] = c;
         sn[t] = s;
-        col_of[2 * t] = p;  // reuse as pair table (col_of no longer needed... keep copy below)
-        col_of[2 * t + 1] = q;
+        pair_ab[t][0] = p;
+        pair_ab[t][1] = q;
       }
       __syncthreads();
       // columns: H <- H J ; Q <- Q J   (for each pair, each row)
       for (int i = t; i < (m / 2) * cnt; i += JT) {
-        int pr = i / cnt, r = i % cnt;
-        int p = col_of[2 * pr], q = col_of[2 * pr + 1];
+        int pr = i / cnt, r = i - pr * cnt;
+        int p = pair_ab[pr][0], q = pair_ab[pr][1];
         if (q >= cnt) continue;
         double c = cs[pr], s = sn[pr];
         double hp = H[r * (JC + 1) + p], hq = H[r * (JC + 1) + q];
@@ -268,8 +330,8 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
       __syncthreads();
       // rows: H <- J^T H
       for (int i = t; i < (m / 2) * cnt; i += JT) {
-        int pr = i / cnt, r = i % cnt;
-        int p = col_of[2 * pr], q = col_of[2 * pr + 1];
+        int pr = i / cnt, r = i - pr * cnt;
+        int p = pair_ab[pr][0], q = pair_ab[pr][1];
         if (q >= cnt) continue;
         double c = cs[pr], s = sn[pr];
         double hp = H[p * (JC + 1) + r], hq = H[q * (JC + 1) + r];
@@ -280,36 +342,25 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
     }
     if (done) break;
   }
-  // restore column ids
-  if (t == 0) {
-    int c = 0;
-    for (int b : {pa, pb}) {
-      if (b < 0) continue;
-      int j0 = b * JB, j1 = min(n, j0 + JB);
-      for (int j = j0; j < j1; j++) col_of[c++] = j;
-    }
-  }
-  __syncthreads();
   // X <- X Q, then V <- V Q (V staged through the same shared buffer).  Rows
   // in parallel; per row JC independent register accumulators (fully unrolled,
   // no local-memory arrays), operands from shared memory (X column-major:
   // consecutive rows -> consecutive banks; Q broadcast).  Unused columns
   // (cnt < JC) carry zeros in Q.
+#pragma unroll 1
   for (int pass = 0; pass < 2; pass++) {
     double* dst = pass == 0 ? Xc : Vc;
     if (pass == 1) {
       __syncthreads();
-      for (int i = t; i < cnt * n; i += JT) {
-        int c = i / n, r = i % n;
-        Xs[(size_t)c * n + r] = Vc[(size_t)col_of[c] * n + r];
-      }
+      load_cols(Xs, Vc, n, cnt, col_of);
       __syncthreads();
     }
+#pragma unroll 1
     for (int r = t; r < n; r += JT) {
       double acc[JC];
 #pragma unroll
       for (int j = 0; j < JC; j++) acc[j] = 0.0;
-#pragma unroll
+#pragma unroll 2
       for (int c = 0; c < JC; c++) {
         const double xv = (c < cnt) ? Xs[(size_t)c * n + r] : 0.0;
 #pragma unroll
@@ -422,44 +473,67 @@ void cholesky_solve(const double* L, int n, double* B, int nrhs, cudaStream_t s)
 // One-sided (Hestenes) block Jacobi on the columns of X (column-major n x n):
 // X W = U Sigma.  Eigenvectors of X^T X are the columns of W (returned row-major
 // in V, eigenvectors in columns); w = Sigma^2 (squared = true) or Sigma.
-static void jacobi_cols(const double* X0, int n, double* V, double* w, bool squared, cudaStream_t s) {
-  DevBuf Xc, Vc;
-  Xc.ensure((size_t)n * n);
-  Vc.ensure((size_t)n * n);
-  GPFVM_CUDA(cudaMemcpyAsync(Xc.ptr, X0, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
-  eye_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(Vc.ptr, n);
-  count_launch();
+template <int JB>
+static int jacobi_sweeps(double* Xc, double* Vc, int n, cudaStream_t s) {
+  constexpr int JC = 2 * JB;
   int nblk = (n + JB - 1) / JB;
   int players = nblk + (nblk & 1);
-  std::vector<std::vector<int>> rounds;
+  std::vector<int> rounds;  // (players - 1) rounds x players entries
   for (int r = 0; r < players - 1; r++) {
-    std::vector<int> pr;
     for (int i = 0; i < players / 2; i++) {
       int a = (i == 0) ? 0 : 1 + ((i - 1 + r) % (players - 1));
       int b = 1 + ((players - 2 - i + r) % (players - 1));
-      pr.push_back(a < nblk ? a : -1);
-      pr.push_back(b < nblk ? b : -1);
+      rounds.push_back(a < nblk ? a : -1);
+      rounds.push_back(b < nblk ? b : -1);
     }
-    rounds.push_back(pr);
   }
-  int* d_pairs = nullptr;
-  unsigned long long* d_off = nullptr;
-  GPFVM_CUDA(cudaMalloc(&d_pairs, sizeof(int) * players * (players - 1) + sizeof(int)));
-  GPFVM_CUDA(cudaMalloc(&d_off, sizeof(unsigned long long)));
-  for (int r = 0; r < players - 1; r++)
-    GPFVM_CUDA(cudaMemcpyAsync(d_pairs + r * players, rounds[r].data(), sizeof(int) * players,
-                               cudaMemcpyHostToDevice, s));
+  DevBuf pairs_buf, off_buf;
+  pairs_buf.ensure((rounds.size() + 1) / 2 + 1);
+  off_buf.ensure(1);
+  int* d_pairs = reinterpret_cast<int*>(pairs_buf.ptr);
+  unsigned long long* d_off = reinterpret_cast<unsigned long long*>(off_buf.ptr);
+  GPFVM_CUDA(cudaMemcpyAsync(d_pairs, rounds.data(), sizeof(int) * rounds.size(), cudaMemcpyHostToDevice, s));
   size_t smem = sizeof(double) * ((size_t)JC * n + 2 * JC * (JC + 1));
-  GPFVM_CHECK(smem <= 227 * 1024, GPFVM_ERR_UNSUPPORTED, "eigensolver: dimension too large (n > 800)");
-  GPFVM_CUDA(cudaFuncSetAttribute(jacobi_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  GPFVM_CHECK(smem <= 220 * 1024, GPFVM_ERR_UNSUPPORTED, "eigensolver: dimension too large");
+  {
+    // The attribute is per function and device, and sygv runs on several host
+    // threads at once with different n: set it once to the maximum (under a
+    // lock) instead of per call, so no thread lowers it under another's launch.
+    static std::mutex mu;
+    static unsigned long long done_mask = 0;
+    int dev = 0;
+    GPFVM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(done_mask >> dev & 1ull)) {
+      int optin = 0;
+      GPFVM_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      cudaFuncAttributes fa;
+      GPFVM_CUDA(cudaFuncGetAttributes(&fa, jacobi_round_kernel<JB>));
+      GPFVM_CUDA(cudaFuncSetAttribute(jacobi_round_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - (int)fa.sharedSizeBytes));
+      done_mask |= 1ull << dev;
+    }
+  }
+  // absolute floor tau ||X||_F^2 (GPFVM_JAC_TAU, default 0 = relative measure)
+  static const double tau = getenv("GPFVM_JAC_TAU") ? atof(getenv("GPFVM_JAC_TAU")) : 0.0;
+  DevBuf fro;
+  const double* d_floor = nullptr;
+  if (tau > 0.0) {
+    fro.ensure(1);
+    dot_many(Xc, (int64_t)n * n, Xc, (int64_t)n * n, 1, fro.ptr, s);
+    scale_scalar(fro.ptr, tau, s);
+    d_floor = fro.ptr;
+  }
+  const double conv_tol = std::max(4e-15, 2e-16 * n);
   int sweeps = 0;
   double offd = 1.0;
-  if (getenv("GPFVM_INNER")) { int v = atoi(getenv("GPFVM_INNER")); GPFVM_CUDA(cudaMemcpyToSymbol(c_inner_sweeps, &v, sizeof(int))); }
+  const bool dbg2 = getenv("GPFVM_DEBUG") && atoi(getenv("GPFVM_DEBUG")) > 1;
   for (int sweep = 0; sweep < 40; sweep++) {
     sweeps++;
     GPFVM_CUDA(cudaMemsetAsync(d_off, 0, sizeof(unsigned long long), s));
     for (int r = 0; r < players - 1; r++) {
-      jacobi_round_kernel<<<players / 2, JT, smem, s>>>(Xc.ptr, Vc.ptr, n, nblk, d_pairs + r * players, d_off);
+      jacobi_round_kernel<JB><<<players / 2, JT, smem, s>>>(Xc, Vc, n, nblk, d_pairs + r * players, d_off,
+                                                             d_floor, sweep > 0 ? conv_tol : 0.0);
       count_launch();
     }
     check_launch("jacobi_round_kernel");
@@ -467,18 +541,37 @@ static void jacobi_cols(const double* X0, int n, double* V, double* w, bool squa
     GPFVM_CUDA(cudaMemcpyAsync(&off, d_off, sizeof(off), cudaMemcpyDeviceToHost, s));
     GPFVM_CUDA(cudaStreamSynchronize(s));
     memcpy(&offd, &off, sizeof(double));
-    if (getenv("GPFVM_DEBUG") && atoi(getenv("GPFVM_DEBUG")) > 1) fprintf(stderr, "[gpfvm]   sweep %d off %.3e\n", sweep, offd);
+    if (dbg2) fprintf(stderr, "[gpfvm]   sweep %d off %.3e\n", sweep, offd);
     // one-sided Jacobi orthogonality floor ~ n eps (rounding of the column dots)
-    if (offd < std::max(4e-15, 2e-16 * n)) break;
+    if (offd < conv_tol) break;
   }
-  if (getenv("GPFVM_DEBUG")) fprintf(stderr, "[gpfvm] jacobi n=%d sweeps=%d offmax=%.3e\n", n, sweeps, offd);
+  if (getenv("GPFVM_DEBUG")) fprintf(stderr, "[gpfvm] jacobi n=%d JB=%d sweeps=%d offmax=%.3e\n", n, JB, sweeps, offd);
+  return sweeps;
+}
+
+// One-sided (Hestenes) block Jacobi on the columns of X (column-major n x n):
+// X W = U Sigma.  Eigenvectors of X^T X are the columns of W (returned row-major
+// in V, eigenvectors in columns); w = Sigma^2 (squared = true) or Sigma.
+// Column-block width JB: 8 for n <= 512 (more CTAs per round: the round is
+// latency-bound, not flop-bound), 16 above (shared memory holds 2*JB columns).
+static void jacobi_cols(const double* X0, int n, double* V, double* w, bool squared, cudaStream_t s) {
+  DevBuf Xc, Vc;
+  Xc.ensure((size_t)n * n);
+  Vc.ensure((size_t)n * n);
+  GPFVM_CUDA(cudaMemcpyAsync(Xc.ptr, X0, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  eye_kernel<<<(unsigned)(((int64_t)n * n + 255) / 256), 256, 0, s>>>(Vc.ptr, n);
+  count_launch();
+  if (getenv("GPFVM_INNER")) { int v = atoi(getenv("GPFVM_INNER")); GPFVM_CUDA(cudaMemcpyToSymbol(c_inner_sweeps, &v, sizeof(int))); }
+  static const int jb_env = getenv("GPFVM_JB") ? atoi(getenv("GPFVM_JB")) : 0;
+  const int jb = jb_env ? jb_env : (n <= 512 ? 8 : 16);
+  if (jb == 4) jacobi_sweeps<4>(Xc.ptr, Vc.ptr, n, s);
+  else if (jb == 8) jacobi_sweeps<8>(Xc.ptr, Vc.ptr, n, s);
+  else jacobi_sweeps<16>(Xc.ptr, Vc.ptr, n, s);
   colnorm_kernel<<<n, 256, 0, s>>>(Xc.ptr, n, w, squared);
   count_launch();
   // Vc is column-major; V row-major with eigenvectors in columns == transpose of Vc storage
   transpose(Vc.ptr, V, n, n, s);
   GPFVM_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_pairs);
-  cudaFree(d_off);
 }
 
 static void sygv_core(const double* A, const double* Bm, int n, double* V, double* w, cudaStream_t s) {
@@ -518,7 +611,7 @@ static void sygv_core(const double* A, const double* Bm, int n, double* V, doubl
 }
 
 namespace {
-// orthonormal trigonometric bases (columns = basis vectors): 1 = DST-I, 2 = DCT-II
+// orthonormal trigonometric bases (columns = basis vectors): 1 = DST-I, 2 = DCT-II, 4 = DCT-IV
 __global__ void trig_basis_kernel(double* S, int n, int kind) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -527,6 +620,8 @@ __global__ void trig_basis_kernel(double* S, int n, int kind) {
   double v;
   if (kind == 1) {
     v = sqrt(2.0 / (n + 1)) * sin(pi * (double)(j + 1) * (double)(k + 1) / (n + 1));
+  } else if (kind == 4) {
+    v = sqrt(2.0 / n) * cos(pi * (j + 0.5) * (k + 0.5) / n);
   } else {
     v = sqrt((k == 0 ? 1.0 : 2.0) / n) * cos(pi * (j + 0.5) * (double)k / n);
   }
@@ -544,17 +639,59 @@ void gemm_rm(const double* A, bool ta, const double* B, bool tb, double* C, int 
   g.C = C; g.c_rs = n; g.c_cs = 1;
   run_gemm(g, s);
 }
+// max |A[i][j] - A[n-1-i][n-1-j]| and max |A[i][j]| (as ordered bit patterns)
+__global__ void centro_kernel(const double* A, int n, unsigned long long* out) {
+  double dev = 0.0, mx = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(idx / n), j = (int)(idx % n);
+    double a = A[idx];
+    dev = fmax(dev, fabs(a - A[(int64_t)(n - 1 - i) * n + (n - 1 - j)]));
+    mx = fmax(mx, fabs(a));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, (unsigned long long)__double_as_longlong(dev));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(mx));
+  }
+}
+
+// Even / odd blocks of a centrosymmetric n x n matrix (n = 2h):
+// E = A11 + A12 J, O = A11 - A12 J  (P^T A P for P = [[I, I], [J, -J]] / sqrt 2).
+__global__ void parity_split_kernel(const double* A, int h, double* E, double* O) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)h * h) return;
+  int i = (int)(idx / h), j = (int)(idx % h);
+  const int n = 2 * h;
+  double a = A[(int64_t)i * n + j], b = A[(int64_t)i * n + (n - 1 - j)];
+  E[idx] = a + b;
+  O[idx] = a - b;
+}
+
+// V = P blockdiag(Ve, Vo): columns c < h symmetric, c >= h antisymmetric.
+__global__ void parity_merge_kernel(const double* Ve, const double* Vo, int h, double* V) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)h * h) return;
+  int i = (int)(idx / h), c = (int)(idx % h);
+  const int n = 2 * h;
+  const double r = 0.70710678118654752440;
+  double e = Ve[idx] * r, o = Vo[idx] * r;
+  V[(int64_t)i * n + c] = e;
+  V[(int64_t)(n - 1 - i) * n + c] = e;
+  V[(int64_t)i * n + h + c] = o;
+  V[(int64_t)(n - 1 - i) * n + h + c] = -o;
+}
 }  // namespace
 
-// A V = Bm V diag(w), V^T Bm V = I.  The pencil is first rotated into an
-// orthonormal trigonometric basis S (DCT-II by default; measured 95 vs 150 ms on config 1): for the Toeplitz-like
-// factor matrices of uniform grids S^T A S and S^T Bm S are nearly diagonal
-// (median off-diagonal correlation ~1e-11), so the Jacobi iteration inside
-// sygv_core needs far fewer sweeps.  Exact for any orthogonal S:
-// A (S V') = Bm (S V') w  and  (S V')^T Bm (S V') = I.
-void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaStream_t s) {
-  static const int basis = getenv("GPFVM_EIG_BASIS") ? atoi(getenv("GPFVM_EIG_BASIS")) : 2;
-  if (basis == 0 || n < 8) {
+// Pencil rotated into the orthonormal trigonometric basis S (kind), solved by
+// sygv_core, rotated back: exact for any orthogonal S.
+static void sygv_rotated(const double* A, const double* Bm, int n, double* V, double* w, int kind,
+                         cudaStream_t s) {
+  static const bool no_rot = getenv("GPFVM_NO_ROT") != nullptr;
+  if (kind == 0 || n < 8 || no_rot) {
     sygv_core(A, Bm, n, V, w, s);
     return;
   }
@@ -562,7 +699,7 @@ void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaSt
   S.ensure((size_t)n * n); T.ensure((size_t)n * n); Ap.ensure((size_t)n * n); Bp.ensure((size_t)n * n);
   Vp.ensure((size_t)n * n);
   unsigned blocks = (unsigned)(((int64_t)n * n + 255) / 256);
-  trig_basis_kernel<<<blocks, 256, 0, s>>>(S.ptr, n, basis);
+  trig_basis_kernel<<<blocks, 256, 0, s>>>(S.ptr, n, kind);
   count_launch();
   gemm_rm(A, false, S.ptr, false, T.ptr, n, s);      // T = A S
   gemm_rm(S.ptr, true, T.ptr, false, Ap.ptr, n, s);  // A' = S^T A S
@@ -573,6 +710,76 @@ void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaSt
   count_launch(2);
   sygv_core(Ap.ptr, Bp.ptr, n, Vp.ptr, w, s);
   gemm_rm(S.ptr, false, Vp.ptr, false, V, n, s);     // V = S V'
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+}
+
+static bool centrosymmetric(const double* A, const double* Bm, int n, cudaStream_t s) {
+  DevBuf buf;
+  buf.ensure(4);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(buf.ptr);
+  GPFVM_CUDA(cudaMemsetAsync(d, 0, 4 * sizeof(unsigned long long), s));
+  int grid = (int)std::min<int64_t>(296, ((int64_t)n * n + 255) / 256);
+  centro_kernel<<<grid, 256, 0, s>>>(A, n, d);
+  centro_kernel<<<grid, 256, 0, s>>>(Bm, n, d + 2);
+  count_launch(2);
+  unsigned long long h[4];
+  GPFVM_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+  double v[4];
+  memcpy(v, h, sizeof(v));
+  return v[0] <= 1e-14 * v[1] && v[2] <= 1e-14 * v[3];
+}
+
+// A V = Bm V diag(w), V^T Bm V = I (generalised symmetric-definite eigenproblem
+// of the FD preconditioner).  Each (sub)pencil is first rotated
+// into an orthonormal trigonometric basis (measured: fewer Jacobi sweeps on the
+// factor matrices of uniform grids, 95 vs 150 ms on config 1 before the parity
+// split); exact for any orthogonal S: A (S V') = Bm (S V') w.
+void sygv(const double* A, const double* Bm, int n, double* V, double* w, cudaStream_t s) {
+  static const int basis = getenv("GPFVM_EIG_BASIS") ? atoi(getenv("GPFVM_EIG_BASIS")) : 2;
+  static const bool no_parity = getenv("GPFVM_NO_PARITY") != nullptr;
+  if (basis == 0 || n < 16 || (n & 1) || no_parity || !centrosymmetric(A, Bm, n, s)) {
+    sygv_rotated(A, Bm, n, V, w, basis, s);
+    return;
+  }
+  // Centrosymmetric pencil (uniform grid, stationary kernel: J A J = A): the
+  // even and odd subspaces decouple exactly, two independent n/2 problems
+  // (1/4 of the Jacobi work each, solved concurrently).  Their trigonometric
+  // bases are the even (DCT-II, size n/2) and odd (DCT-IV, size n/2) halves
+  // of the size-n DCT-II.
+  const int h = n / 2;
+  DevBuf Ae, Ao, Be, Bo, Ve, Vo;
+  for (DevBuf* b : {&Ae, &Ao, &Be, &Bo, &Ve, &Vo}) b->ensure((size_t)h * h);
+  unsigned blocks = (unsigned)(((int64_t)h * h + 255) / 256);
+  parity_split_kernel<<<blocks, 256, 0, s>>>(A, h, Ae.ptr, Ao.ptr);
+  parity_split_kernel<<<blocks, 256, 0, s>>>(Bm, h, Be.ptr, Bo.ptr);
+  count_launch(2);
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+  cudaStream_t so;
+  GPFVM_CUDA(cudaStreamCreateWithFlags(&so, cudaStreamNonBlocking));
+  int dev = 0;
+  GPFVM_CUDA(cudaGetDevice(&dev));
+  Error err{GPFVM_OK, ""};
+  std::thread th([&] {
+    try {
+      cudaSetDevice(dev);
+      sygv_rotated(Ao.ptr, Bo.ptr, h, Vo.ptr, w + h, basis == 2 ? 4 : basis, so);
+    } catch (const Error& e) {
+      err = e;
+    }
+  });
+  try {
+    sygv_rotated(Ae.ptr, Be.ptr, h, Ve.ptr, w, basis, s);
+  } catch (...) {
+    th.join();
+    cudaStreamDestroy(so);
+    throw;
+  }
+  th.join();
+  cudaStreamDestroy(so);
+  if (err.code != GPFVM_OK) throw err;
+  parity_merge_kernel<<<blocks, 256, 0, s>>>(Ve.ptr, Vo.ptr, h, V);
+  count_launch();
   GPFVM_CUDA(cudaStreamSynchronize(s));
 }
 
