@@ -104,30 +104,15 @@ double now_ms() {
 }  // namespace
 
 // FD apply on R vectors (stride ldx in, ldy out), x != y
-static void fd_apply(Precond& pc, const double* x, int64_t ldx, double* y, int64_t ldy, int R, cudaStream_t s) {
+// Second half of FD: y_r = (V (x) W) D^{-1} t_r for R vectors t_r stored in
+// pc.t2 (stride Np, overwritten).
+static void fd_backward(Precond& pc, double* y, int64_t ldy, int R, cudaStream_t s) {
   const int n0 = pc.n0, n1 = pc.n1;
   const int64_t np = pc.Np;
-  pc.t1.ensure((size_t)np * R);
-  pc.t2.ensure((size_t)np * R);
-  Gemm g;
-  // T1_r = X_r W
-  g = Gemm();
-  g.M = n0; g.N = n1; g.K = n1; g.batch1 = R;
-  g.A = x; g.a_rs = n1; g.a_cs = 1; g.a_b1 = ldx;
-  g.B = pc.W.ptr; g.b_rs = n1; g.b_cs = 1;
-  g.C = pc.t1.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
-  run_gemm(g, s);
-  // T2_r = V^T T1_r
-  g = Gemm();
-  g.M = n0; g.N = n1; g.K = n0; g.batch1 = R;
-  g.A = pc.Vt.ptr; g.a_rs = n0; g.a_cs = 1;
-  g.B = pc.t1.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = np;
-  g.C = pc.t2.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
-  run_gemm(g, s);
   scale_cols_kernel<<<dim3(std::min<unsigned>(g1(np), 1184), R), 256, 0, s>>>(pc.t2.ptr, pc.Dinv.ptr, np, R, np);
   count_launch();
+  Gemm g;
   // T1_r = V T2_r
-  g = Gemm();
   g.M = n0; g.N = n1; g.K = n0; g.batch1 = R;
   g.A = pc.V.ptr; g.a_rs = n0; g.a_cs = 1;
   g.B = pc.t2.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = np;
@@ -140,6 +125,29 @@ static void fd_apply(Precond& pc, const double* x, int64_t ldx, double* y, int64
   g.B = pc.W.ptr; g.b_rs = 1; g.b_cs = n1;
   g.C = y; g.c_rs = n1; g.c_cs = 1; g.c_b1 = ldy;
   run_gemm(g, s);
+}
+
+// y_r = FD x_r = (V (x) W) D^{-1} (V (x) W)^T x_r
+static void fd_apply(Precond& pc, const double* x, int64_t ldx, double* y, int64_t ldy, int R, cudaStream_t s) {
+  const int n0 = pc.n0, n1 = pc.n1;
+  const int64_t np = pc.Np;
+  pc.t1.ensure((size_t)np * R);
+  pc.t2.ensure((size_t)np * R);
+  Gemm g;
+  // T1_r = X_r W
+  g.M = n0; g.N = n1; g.K = n1; g.batch1 = R;
+  g.A = x; g.a_rs = n1; g.a_cs = 1; g.a_b1 = ldx;
+  g.B = pc.W.ptr; g.b_rs = n1; g.b_cs = 1;
+  g.C = pc.t1.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
+  run_gemm(g, s);
+  // T2_r = V^T T1_r
+  g = Gemm();
+  g.M = n0; g.N = n1; g.K = n0; g.batch1 = R;
+  g.A = pc.Vt.ptr; g.a_rs = n0; g.a_cs = 1;
+  g.B = pc.t1.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = np;
+  g.C = pc.t2.ptr; g.c_rs = n1; g.c_cs = 1; g.c_b1 = np;
+  run_gemm(g, s);
+  fd_backward(pc, y, ldy, R, s);
 }
 
 static const KronTerm* find_term(gpfvm_problem* p, int I, int J, int fid0, int fid1) {
@@ -224,9 +232,9 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   GPFVM_CHECK(pc.nb <= 16384, GPFVM_ERR_UNSUPPORTED, "block-LDL: more than 16384 deflated observations");
   const int nb = (int)pc.nb;
   const int64_t np = pc.Np;
-  pc.GpbT.ensure((size_t)nb * np);
   pc.YT.ensure((size_t)nb * np);
   DevBuf S, S0, eye, Lf;
+  PhaseTimer pt(s);
   S.ensure((size_t)nb * nb);
   fill(S.ptr, 0.0, (int64_t)nb * nb, s);
   // identity right-hand sides per deflated block, pushed through the Kronecker terms
@@ -236,14 +244,6 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     eye.ensure((size_t)nJ * nJ);
     set_identity_kernel<<<g1((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
     count_launch();
-    // rows of G_pb^T : (G_{P,J} e_c)^T
-    {
-      std::vector<const KronTerm*> ts;
-      for (const auto& t : p->terms)
-        if (t.I == pc.P && t.J == J) ts.push_back(&t);
-      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[pc.P].shape, eye.ptr, nJ,
-                  pc.GpbT.ptr + pc.boff[jb] * np, np, nJ, true, s, p->ws);
-    }
     for (size_t ib = 0; ib < pc.bblocks.size(); ib++) {
       const int I = pc.bblocks[ib];
       std::vector<const KronTerm*> ts;
@@ -255,8 +255,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
                   S.ptr + pc.boff[jb] * nb + pc.boff[ib], nb, nJ, true, s, p->ws);
     }
   }
-  PhaseTimer pt(s);
-  pt.mark("ldl: Gpb/Gbb from identities");
+  pt.mark("ldl: Gbb from identities");
   // noise on the diagonal of G_bb
   {
     std::vector<double> nz(nb);
@@ -271,18 +270,112 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     count_launch();
     GPFVM_CUDA(cudaStreamSynchronize(s));
   }
-  // Y^T = FD(G_pb) rows
-  fd_apply(pc, pc.GpbT.ptr, np, pc.YT.ptr, np, nb, s);
-  pt.mark("ldl: Y = FD(Gpb)");
-  // S = G_bb - G_pb^T Y
+  // Y^T = FD(G_pb) rows without forming G_pb: per deflated block J,
+  // (V (x) W)^T G_{P,J} = sum_tau c_tau (V^T F0_tau) (x) (W^T F1_tau) is again a
+  // Kronecker sum with small factors, applied to the identity of block J; then
+  // the D^{-1} scale and the (V (x) W) half of FD.
   {
-    Gemm g;
-    g.M = nb; g.N = nb; g.K = (int)np;
-    g.A = pc.GpbT.ptr; g.a_rs = np; g.a_cs = 1;
-    g.B = pc.YT.ptr; g.b_rs = 1; g.b_cs = np;
-    g.C = S.ptr; g.c_rs = nb; g.c_cs = 1;
-    g.alpha = -1.0; g.beta = 1.0;
-    run_gemm(g, s);
+    const int n0 = pc.n0, n1 = pc.n1;
+    std::vector<DevBuf> rot;
+    DevBuf w0, w1;
+    for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+      const int J = pc.bblocks[jb];
+      const int nJ = (int)p->blocks[J].size;
+      std::vector<double> coefs;
+      std::vector<std::vector<const double*>> fs;
+      for (const auto& t : p->terms) {
+        if (t.I != pc.P || t.J != J) continue;
+        const Factor& F0 = p->factors[t.fid[0]];
+        const Factor& F1 = p->factors[t.fid[1]];
+        DevBuf R0, R1;
+        R0.ensure((size_t)n0 * F0.cols);
+        R1.ensure((size_t)n1 * F1.cols);
+        Gemm g;  // R0 = V^T F0
+        g.M = n0; g.N = F0.cols; g.K = n0;
+        g.A = pc.Vt.ptr; g.a_rs = n0; g.a_cs = 1;
+        g.B = F0.data.ptr; g.b_rs = F0.cols; g.b_cs = 1;
+        g.C = R0.ptr; g.c_rs = F0.cols; g.c_cs = 1;
+        run_gemm(g, s);
+        g = Gemm();  // R1 = W^T F1
+        g.M = n1; g.N = F1.cols; g.K = n1;
+        g.A = pc.W.ptr; g.a_rs = 1; g.a_cs = n1;
+        g.B = F1.data.ptr; g.b_rs = F1.cols; g.b_cs = 1;
+        g.C = R1.ptr; g.c_rs = F1.cols; g.c_cs = 1;
+        run_gemm(g, s);
+        coefs.push_back(t.coef);
+        fs.push_back({R0.ptr, R1.ptr});
+        rot.push_back(std::move(R0));
+        rot.push_back(std::move(R1));
+      }
+      pc.t1.ensure((size_t)np * nJ);
+      pc.t2.ensure((size_t)np * nJ);
+      if (coefs.empty()) {
+        fill(pc.YT.ptr + pc.boff[jb] * np, 0.0, (int64_t)nJ * np, s);
+        continue;
+      }
+      eye.ensure((size_t)nJ * nJ);
+      set_identity_kernel<<<g1((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
+      count_launch();
+      KronSum ks;
+      ks.build(p->ndim, p->blocks[J].shape, p->blocks[pc.P].shape, coefs, fs, s);
+      const int64_t wsz = std::max<int64_t>(1, ks.workspace_per_rhs()) * nJ;
+      w0.ensure((size_t)wsz);
+      w1.ensure((size_t)wsz);
+      ks.apply(eye.ptr, nJ, pc.t2.ptr, np, nJ, 0.0, w0.ptr, w1.ptr, s);
+      fd_backward(pc, pc.YT.ptr + pc.boff[jb] * np, np, nJ, s);
+    }
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  }
+  pt.mark("ldl: Y = FD(Gpb)");
+  // G_{I,P} Kronecker sums (used by P^{-1})
+  pc.ks_bp.clear();
+  pc.ks_bp.resize(pc.bblocks.size());
+  {
+    int64_t wmax = 1;
+    for (size_t ib = 0; ib < pc.bblocks.size(); ib++) {
+      const int I = pc.bblocks[ib];
+      std::vector<double> coefs;
+      std::vector<std::vector<const double*>> fs;
+      for (const auto& t : p->terms) {
+        if (t.I != I || t.J != pc.P) continue;
+        coefs.push_back(t.coef);
+        std::vector<const double*> f;
+        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        fs.push_back(f);
+      }
+      pc.ks_bp[ib].build(p->ndim, p->blocks[pc.P].shape, p->blocks[I].shape, coefs, fs, s);
+      wmax = std::max(wmax, pc.ks_bp[ib].workspace_per_rhs());
+    }
+    pc.kw0.ensure((size_t)wmax);
+    pc.kw1.ensure((size_t)wmax);
+  }
+  // S = G_bb - G_bp Y: instead of the dense GEMM with G_pb^T (nb x nb x N_PDE
+  // flops) apply each Kronecker sum -G_{I,P} to the nb columns of Y, contracted
+  // in its cheapest mode order (IC/BC blocks are thin in one dimension: ~100x
+  // fewer flops on config 1).  Row c of S receives (G_{I,P} y_c)^T; S is
+  // symmetrised below.
+  {
+    DevBuf w0, w1;
+    for (size_t ib = 0; ib < pc.bblocks.size(); ib++) {
+      const int I = pc.bblocks[ib];
+      std::vector<double> coefs;
+      std::vector<std::vector<const double*>> fs;
+      for (const auto& t : p->terms) {
+        if (t.I != I || t.J != pc.P) continue;
+        coefs.push_back(-t.coef);
+        std::vector<const double*> f;
+        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        fs.push_back(f);
+      }
+      if (coefs.empty()) continue;
+      KronSum ks;
+      ks.build(p->ndim, p->blocks[pc.P].shape, p->blocks[I].shape, coefs, fs, s);
+      const int64_t wsz = std::max<int64_t>(1, ks.workspace_per_rhs()) * nb;
+      w0.ensure((size_t)wsz);
+      w1.ensure((size_t)wsz);
+      ks.apply(pc.YT.ptr, np, S.ptr + pc.boff[ib], nb, nb, 1.0, w0.ptr, w1.ptr, s);
+    }
+    GPFVM_CUDA(cudaStreamSynchronize(s));
   }
   symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(S.ptr, nb);
   count_launch();
@@ -399,7 +492,9 @@ void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s)
     const BlockInt& B = p->blocks[pc.bblocks[jb]];
     copy(pc.rb.ptr + pc.boff[jb], r + B.offset, B.size, s);
   }
-  dot_many(pc.GpbT.ptr, pc.Np, zp, pc.Np, nb, pc.cvec.ptr, s);  // G_pb^T FD r_p
+  for (size_t ib = 0; ib < pc.bblocks.size(); ib++)  // c = G_bp FD r_p
+    pc.ks_bp[ib].apply(zp, pc.Np, pc.cvec.ptr + pc.boff[ib], p->blocks[pc.bblocks[ib]].size, 1, 0.0,
+                       pc.kw0.ptr, pc.kw1.ptr, s);
   sub_kernel<<<g1(nb), 256, 0, s>>>(pc.rb.ptr, pc.cvec.ptr, nb);
   count_launch();
   dot_many(pc.Sinv.ptr, nb, pc.rb.ptr, nb, nb, pc.zb.ptr, s);    // z_b = S^{-1} t
