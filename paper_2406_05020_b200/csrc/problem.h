@@ -68,7 +68,7 @@ struct Precond {
   std::vector<int> bblocks;
   std::vector<int64_t> boff;  // offset of each deflated block inside the b-vector
   int64_t nb = 0;
-  DevBuf YT, Sinv;                 // Y^T = (FD G_pb)^T (nb x Np), explicit S^{-1}
+  DevBuf YT, Sinv, Linv;           // Y^T = (FD G_pb)^T (nb x Np), explicit S^{-1} = L^{-T} L^{-1}
   std::vector<KronSum> ks_bp;      // G_{I,P} per deflated block I (Kronecker sums)
   DevBuf kw0, kw1;                 // their workspaces (one vector)
   double shift = 0.0;

@@ -412,12 +412,22 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   }
   cudaFree(d_info);
   pc.shift = shift;
-  // explicit S^{-1} (nb x nb) so each application is one multi-dot
-  pc.Sinv.ensure((size_t)nb * nb);
-  set_identity_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb, nb);
-  count_launch();
+  // explicit L^{-1} (lower triangular; the PRECOND variance uses ||L^{-1} z||^2)
+  // and S^{-1} = L^{-T} L^{-1} (nb x nb) so each application is one multi-dot
   pt.mark("ldl: cholesky(S)");
-  cholesky_solve(Lf.ptr, nb, pc.Sinv.ptr, nb, s);
+  pc.Linv.ensure((size_t)nb * nb);
+  set_identity_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Linv.ptr, nb, nb);
+  count_launch();
+  trsm_lower(Lf.ptr, nb, pc.Linv.ptr, nb, s);
+  pc.Sinv.ensure((size_t)nb * nb);
+  {
+    Gemm g;
+    g.M = nb; g.N = nb; g.K = nb;
+    g.A = pc.Linv.ptr; g.a_rs = 1; g.a_cs = nb;  // L^{-T}
+    g.B = pc.Linv.ptr; g.b_rs = nb; g.b_cs = 1;
+    g.C = pc.Sinv.ptr; g.c_rs = nb; g.c_cs = 1;
+    run_gemm(g, s);
+  }
   pt.mark("ldl: S^{-1}");
   symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(pc.Sinv.ptr, nb);
   count_launch();
