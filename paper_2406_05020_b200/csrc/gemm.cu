@@ -272,6 +272,119 @@ __global__ void dgemm_skinny_kernel(Gemm g) {
   }
 }
 
+// Few-row GEMM with a row-major B (b_cs == 1): C[m, n] = alpha sum_k A[m, k] B[k, n]
+// (+ beta C), M <= 8.  One thread per output column n: consecutive threads read
+// consecutive B elements (coalesced rows), A is broadcast; 8 rows of B in
+// flight per thread.  E.g. the time-point functional of an IC block applied to
+// a PDE-shaped vector (K = n_t, N = n_x).
+template <int MM>
+__global__ void __launch_bounds__(256) dgemm_gemvt_kernel(Gemm g) {
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  const int64_t ncol_blocks = (g.N + blockDim.x - 1) / blockDim.x;
+  for (int64_t w = blockIdx.x; w < nbatch * ncol_blocks; w += gridDim.x) {
+    const int64_t z = w / ncol_blocks;
+    const int n = (int)((w - z * ncol_blocks) * blockDim.x + threadIdx.x);
+    if (n >= g.N) continue;
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3 + n;
+    double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3 + (int64_t)n * g.c_cs;
+    double acc[MM];
+#pragma unroll
+    for (int m = 0; m < MM; m++) acc[m] = 0.0;
+    for (int seg = 0; seg < g.nseg; seg++) {
+      const double* As = A + seg * g.a_sg;
+      const double* Bs = B + seg * g.b_sg;
+      int k = 0;
+      for (; k + 8 <= g.K; k += 8) {
+        double bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) bv[u] = __ldg(Bs + (int64_t)(k + u) * g.b_rs);
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+#pragma unroll
+          for (int m = 0; m < MM; m++)
+            if (m < g.M) acc[m] = fma(__ldg(As + (int64_t)m * g.a_rs + (int64_t)(k + u) * g.a_cs), bv[u], acc[m]);
+      }
+      for (; k < g.K; k++) {
+        const double bv = __ldg(Bs + (int64_t)k * g.b_rs);
+#pragma unroll
+        for (int m = 0; m < MM; m++)
+          if (m < g.M) acc[m] = fma(__ldg(As + (int64_t)m * g.a_rs + (int64_t)k * g.a_cs), bv, acc[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MM; m++)
+      if (m < g.M) {
+        double* cp = C + (int64_t)m * g.c_rs;
+        double v = g.alpha * acc[m];
+        if (g.beta != 0.0) v += g.beta * *cp;
+        *cp = v;
+      }
+  }
+}
+
+// Few-column GEMM with A contiguous along K (a_cs == 1): C[m, n] for N <= 8.
+// One warp per output row m computes all N columns, so each row of A is read
+// once (lanes along K, coalesced), 4 rows of A in flight per lane.  E.g. the
+// space-point functionals of BC blocks applied to a PDE-shaped vector.
+template <int NN>
+__global__ void __launch_bounds__(256) dgemm_gemvn_kernel(Gemm g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < nbatch * g.M; w += warps) {
+    const int64_t z = w / g.M;
+    const int m = (int)(w - z * g.M);
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3 + (int64_t)m * g.a_rs;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3;
+    double acc[NN];
+#pragma unroll
+    for (int n = 0; n < NN; n++) acc[n] = 0.0;
+    for (int seg = 0; seg < g.nseg; seg++) {
+      const double* As = A + seg * g.a_sg;
+      const double* Bs = B + seg * g.b_sg;
+      int k = lane;
+      for (; k + 96 < g.K; k += 128) {
+        double av[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) av[u] = __ldg(As + k + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int n = 0; n < NN; n++)
+            if (n < g.N) acc[n] = fma(av[u], __ldg(Bs + (int64_t)(k + 32 * u) * g.b_rs + (int64_t)n * g.b_cs), acc[n]);
+      }
+      for (; k < g.K; k += 32) {
+        const double av = __ldg(As + k);
+#pragma unroll
+        for (int n = 0; n < NN; n++)
+          if (n < g.N) acc[n] = fma(av, __ldg(Bs + (int64_t)k * g.b_rs + (int64_t)n * g.b_cs), acc[n]);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NN; n++) {
+      double v = acc[n];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[n] = v;
+    }
+    if (lane == 0) {
+      double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3 + (int64_t)m * g.c_rs;
+#pragma unroll
+      for (int n = 0; n < NN; n++)
+        if (n < g.N) {
+          double* cp = C + (int64_t)n * g.c_cs;
+          double v = g.alpha * acc[n];
+          if (g.beta != 0.0) v += g.beta * *cp;
+          *cp = v;
+        }
+    }
+  }
+}
+
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool B_ROW, bool V16>
 void launch_dmma(const Gemm& g, cudaStream_t s) {
   using L = SmemLayout<BM, BN, B_ROW>;
@@ -341,6 +454,28 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
   if (!fast) {
     int64_t total = (int64_t)g.M * g.N;
     const int64_t kk = (int64_t)g.K * g.nseg;
+    static const bool no_gemvt = getenv("GPFVM_NO_GEMVT") != nullptr;
+    if (!no_gemvt && g.b_cs == 1 && g.M <= 8 && g.N >= 64 && kk >= 8) {
+      const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+      const int64_t work = nbatch * ((g.N + 127) / 128);
+      const unsigned grid = (unsigned)std::min<int64_t>(work, 148 * 32);
+      if (g.M <= 2) dgemm_gemvt_kernel<2><<<grid, 128, 0, s>>>(g);
+      else if (g.M <= 4) dgemm_gemvt_kernel<4><<<grid, 128, 0, s>>>(g);
+      else dgemm_gemvt_kernel<8><<<grid, 128, 0, s>>>(g);
+      count_launch();
+      check_launch("dgemm_gemvt_kernel");
+      return;
+    }
+    if (!no_gemvt && g.a_cs == 1 && g.N <= 8 && g.M >= 32 && kk >= 64) {
+      const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+      const unsigned grid = (unsigned)std::min<int64_t>((nbatch * g.M + 7) / 8, 148 * 16);
+      if (g.N <= 2) dgemm_gemvn_kernel<2><<<grid, 256, 0, s>>>(g);
+      else if (g.N <= 4) dgemm_gemvn_kernel<4><<<grid, 256, 0, s>>>(g);
+      else dgemm_gemvn_kernel<8><<<grid, 256, 0, s>>>(g);
+      count_launch();
+      check_launch("dgemm_gemvn_kernel");
+      return;
+    }
     if (kk >= 32 && total <= (1 << 20)) {
       const int threads = 256;  // 8 warps, one output each
       unsigned bx = (unsigned)std::min<int64_t>((total + 7) / 8, 4096);
