@@ -50,13 +50,6 @@ __global__ void coldot_sub_kernel(double* var, const double* __restrict__ Z, con
   }
 }
 
-__global__ void set_identity_kernel2(double* X, int n, int64_t ld) {
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n * n) return;
-  int r = (int)(idx / n), c = (int)(idx % n);
-  X[r * ld + c] = (r == c) ? 1.0 : 0.0;
-}
-
 unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
 
 }  // namespace
@@ -212,40 +205,38 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
       run_gemm(g, s);
     }
   // --- IC/BC Schur part ----------------------------------------------------
+  // z(x) = k_b(x) - Y^T k_p(x), var -= z^T S^{-1} z = ||L^{-1} z||^2.  By
+  // linearity L^{-1} Z = K_{*b} L^{-T} - K_{*P} (L^{-1} Y^T)^T: push the rows of
+  // L^{-1} (per deflated block) and of L^{-1} Y^T (cached per preconditioner)
+  // through the cross-covariance Kronecker sums, then column sums of squares.
   if (pc.nb == 0) return;
   const int nb = (int)pc.nb;
-  DevBuf Z, T, eye;
-  Z.ensure((size_t)nb * ng);
-  T.ensure((size_t)nb * ng);
-  // Z rows for deflated block J: K_{*J} e_l
-  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
-    const int J = pc.bblocks[jb];
-    const int nJ = (int)p->blocks[J].size;
-    eye.ensure((size_t)nJ * nJ);
-    set_identity_kernel2<<<gs((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
-    count_launch();
-    if (cp.terms[J].empty()) {
-      for (int r = 0; r < nJ; r++) fill(Z.ptr + (pc.boff[jb] + r) * ng, 0.0, ng, s);
-    } else {
-      cross_apply(p, cp, J, 1.0, eye.ptr, nJ, Z.ptr + pc.boff[jb] * ng, ng, nJ, 0.0, s);
+  if (!pc.LYT.ptr) {
+    // L^{-1} Y^T with L^{-1} lower triangular: row panels touch only the
+    // nonzero columns
+    pc.LYT.ensure((size_t)nb * pc.Np);
+    constexpr int RB = 128;
+    for (int i0 = 0; i0 < nb; i0 += RB) {
+      const int rb = std::min(RB, nb - i0);
+      Gemm g;
+      g.M = rb; g.N = (int)pc.Np; g.K = i0 + rb;
+      g.A = pc.Linv.ptr + (int64_t)i0 * nb; g.a_rs = nb; g.a_cs = 1;
+      g.B = pc.YT.ptr; g.b_rs = pc.Np; g.b_cs = 1;
+      g.C = pc.LYT.ptr + (int64_t)i0 * pc.Np; g.c_rs = pc.Np; g.c_cs = 1;
+      run_gemm(g, s);
     }
   }
-  // Z -= K_{*P} Y  (rows of Y^T through the P cross terms, negated)
-  cross_apply(p, cp, pc.P, -1.0, pc.YT.ptr, pc.Np, Z.ptr, ng, nb, 1.0, s);
-  // z^T S^{-1} z = ||L^{-1} z||^2: T = L^{-1} Z with L^{-1} lower triangular,
-  // as row panels of 128 that only touch the nonzero columns (about half the
-  // flops of the dense S^{-1} Z product); var -= colsum(T o T)
-  constexpr int RB = 128;
-  for (int i0 = 0; i0 < nb; i0 += RB) {
-    const int rb = std::min(RB, nb - i0);
-    Gemm g;
-    g.M = rb; g.N = (int)ng; g.K = i0 + rb;
-    g.A = pc.Linv.ptr + (int64_t)i0 * nb; g.a_rs = nb; g.a_cs = 1;
-    g.B = Z.ptr; g.b_rs = ng; g.b_cs = 1;
-    g.C = T.ptr + (int64_t)i0 * ng; g.c_rs = ng; g.c_cs = 1;
-    run_gemm(g, s);
+  DevBuf Z;
+  Z.ensure((size_t)nb * ng);
+  bool first = true;
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const int J = pc.bblocks[jb];
+    if (cp.terms[J].empty()) continue;
+    cross_apply(p, cp, J, 1.0, pc.Linv.ptr + pc.boff[jb], nb, Z.ptr, ng, nb, first ? 0.0 : 1.0, s);
+    first = false;
   }
-  coldot_sub_kernel<<<gs(ng), 256, 0, s>>>(var, T.ptr, T.ptr, nb, ng);
+  cross_apply(p, cp, pc.P, -1.0, pc.LYT.ptr, pc.Np, Z.ptr, ng, nb, first ? 0.0 : 1.0, s);
+  coldot_sub_kernel<<<gs(ng), 256, 0, s>>>(var, Z.ptr, Z.ptr, nb, ng);
   count_launch();
 }
 

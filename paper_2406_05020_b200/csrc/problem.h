@@ -69,6 +69,7 @@ struct Precond {
   std::vector<int64_t> boff;  // offset of each deflated block inside the b-vector
   int64_t nb = 0;
   DevBuf YT, Sinv, Linv;           // Y^T = (FD G_pb)^T (nb x Np), explicit S^{-1} = L^{-T} L^{-1}
+  DevBuf LYT;                      // L^{-1} Y^T (nb x Np), built on the first PRECOND predict
   std::vector<KronSum> ks_bp;      // G_{I,P} per deflated block I (Kronecker sums)
   DevBuf kw0, kw1;                 // their workspaces (one vector)
   double shift = 0.0;
