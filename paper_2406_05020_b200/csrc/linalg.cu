@@ -268,15 +268,20 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
   const double flo = floor_ptr ? *floor_ptr : 0.0;
   __shared__ double mcta;
   if (t < 32) {
+    // squared correlations (one reciprocal per pair, one sqrt per CTA: FP64
+    // division and sqrt are long multi-instruction sequences on this path)
     double m = 0.0;
+    const double flo2 = flo * flo;
     for (int i = t; i < cnt * cnt; i += 32) {
-      int a = i / cnt, b = i % cnt;
+      int a = i / cnt, b = i - (i / cnt) * cnt;
       if (b <= a) continue;
-      double d = fmax(sqrt(fabs(H[a * (JC + 1) + a]) * fabs(H[b * (JC + 1) + b])), flo);
-      double v = (d > 0.0) ? fabs(H[a * (JC + 1) + b]) / d : 0.0;
+      double d2 = fmax(fabs(H[a * (JC + 1) + a] * H[b * (JC + 1) + b]), flo2);
+      double hab = H[a * (JC + 1) + b];
+      double v = (d2 > 0.0) ? hab * hab * __drcp_rn(d2) : 0.0;
       m = fmax(m, v);
     }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    m = sqrt(m);
     if (t == 0) {
       atomicMax(offmax, (unsigned long long)__double_as_longlong(m));
       mcta = m;
@@ -300,10 +305,13 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
         double c = 1.0, s = 0.0;
         if (q < cnt) {
           double hpp = H[p * (JC + 1) + p], hqq = H[q * (JC + 1) + q], hpq = H[p * (JC + 1) + q];
-          if (fabs(hpq) > 1e-300 && fabs(hpq) > 1e-16 * sqrt(fabs(hpp * hqq)) && fabs(hpq) > 1e-16 * flo) {
-            double zeta = (hqq - hpp) / (2.0 * hpq);
-            double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            c = 1.0 / sqrt(1.0 + tt * tt);
+          // rotate unless |h_pq| <= 1e-16 sqrt(h_pp h_qq) (compared squared);
+          // rotation from reciprocals and one rsqrt: only orthogonality
+          // (c^2 + s^2 = 1 to rounding) matters, not correctly rounded c, s
+          if (fabs(hpq) > 1e-300 && hpq * hpq > 1e-32 * fabs(hpp * hqq) && fabs(hpq) > 1e-16 * flo) {
+            double zeta = (hqq - hpp) * 0.5 * __drcp_rn(hpq);
+            double tt = copysign(__drcp_rn(fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+            c = rsqrt(fma(tt, tt, 1.0));
             s = c * tt;
             done = 0;
           }
