@@ -14,6 +14,7 @@
 // tensor-core instruction of sm_100a; tcgen05 has no f64 kind).  Shared rows
 // are padded so fragment loads hit each 8-byte bank pair exactly twice per
 // warp (2 wavefronts, the minimum for 256 B).
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 
@@ -447,7 +448,26 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
     g.batch1 = 1;
     g.a_b1 = g.c_b1 = 0;
   }
+  // Symmetric case: a single-column GEMM batched over right-hand sides that
+  // share A (e.g. the time factor of a BC block applied to per-vector
+  // contractions) is C^T = B^T A^T with the batch as M — one DMMA GEMM that
+  // reads A once instead of once per vector.
+  if (g.N == 1 && g.batch1 > 1 && g.batch2 == 1 && g.batch3 == 1 && g.a_b1 == 0) {
+    Gemm t = g;
+    t.M = g.batch1; t.N = g.M; t.K = g.K;
+    t.A = g.B; t.a_rs = g.b_b1; t.a_cs = g.b_rs; t.a_sg = g.b_sg;
+    t.B = g.A; t.b_rs = g.a_cs; t.b_cs = g.a_rs; t.b_sg = g.a_sg;
+    t.C = g.C; t.c_rs = g.c_b1; t.c_cs = g.c_rs;
+    t.batch1 = 1;
+    t.a_b1 = t.b_b1 = t.c_b1 = 0;
+    g = t;
+  }
   if (g.M <= 0 || g.N <= 0 || g.batch1 <= 0 || g.batch2 <= 0 || g.batch3 <= 0) return;
+  static const bool trace = getenv("GPFVM_TRACE_GEMM") != nullptr;
+  if (trace)
+    fprintf(stderr, "[gemm] M=%d N=%d K=%d nseg=%d batch=%d,%d,%d a(rs=%lld cs=%lld) b(rs=%lld cs=%lld) c(rs=%lld cs=%lld) beta=%g\n",
+            g.M, g.N, g.K, g.nseg, g.batch1, g.batch2, g.batch3, (long long)g.a_rs, (long long)g.a_cs, (long long)g.b_rs,
+            (long long)g.b_cs, (long long)g.c_rs, (long long)g.c_cs, g.beta);
   GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
                     g.N >= 8 && g.K * g.nseg >= 4;
