@@ -386,6 +386,81 @@ __global__ void __launch_bounds__(256) dgemm_gemvn_kernel(Gemm g) {
   }
 }
 
+// gemvt for 16-byte aligned B with even N and row stride: a 256-thread block
+// covers 64 columns (double2 per thread) x 8 K-slices (one warp each), 8 rows
+// in flight per thread, partial sums reduced through shared memory.
+template <int MM>
+__global__ void __launch_bounds__(256) dgemm_gemvt2_kernel(Gemm g) {
+  __shared__ double2 red[8][MM][32];
+  const int lane = threadIdx.x & 31, ks = threadIdx.x >> 5;
+  const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+  const int64_t ctiles = (g.N + 63) / 64;
+  const int kchunk = (g.K + 7) / 8;
+  const int k0 = ks * kchunk, k1 = min(g.K, k0 + kchunk);
+  for (int64_t w = blockIdx.x; w < nbatch * ctiles; w += gridDim.x) {
+    const int64_t z = w / ctiles;
+    const int n = (int)((w - z * ctiles) * 64 + 2 * lane);
+    const int64_t b1 = z % g.batch1, b23 = z / g.batch1;
+    const int64_t b2 = b23 % g.batch2, b3 = b23 / g.batch2;
+    const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2 + b3 * g.a_b3;
+    const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2 + b3 * g.b_b3 + n;
+    double2 acc[MM];
+#pragma unroll
+    for (int m = 0; m < MM; m++) acc[m] = make_double2(0.0, 0.0);
+    if (n < g.N) {
+      for (int seg = 0; seg < g.nseg; seg++) {
+        const double* As = A + seg * g.a_sg;
+        const double* Bs = B + seg * g.b_sg;
+        int k = k0;
+        for (; k + 8 <= k1; k += 8) {
+          double2 bv[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) bv[u] = __ldg(reinterpret_cast<const double2*>(Bs + (int64_t)(k + u) * g.b_rs));
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+#pragma unroll
+            for (int m = 0; m < MM; m++)
+              if (m < g.M) {
+                const double a = __ldg(As + (int64_t)m * g.a_rs + (int64_t)(k + u) * g.a_cs);
+                acc[m].x = fma(a, bv[u].x, acc[m].x);
+                acc[m].y = fma(a, bv[u].y, acc[m].y);
+              }
+        }
+        for (; k < k1; k++) {
+          const double2 bv = __ldg(reinterpret_cast<const double2*>(Bs + (int64_t)k * g.b_rs));
+#pragma unroll
+          for (int m = 0; m < MM; m++)
+            if (m < g.M) {
+              const double a = __ldg(As + (int64_t)m * g.a_rs + (int64_t)k * g.a_cs);
+              acc[m].x = fma(a, bv.x, acc[m].x);
+              acc[m].y = fma(a, bv.y, acc[m].y);
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MM; m++) red[ks][m][lane] = acc[m];
+    __syncthreads();
+    if (ks < MM && ks < g.M && n < g.N) {
+      double2 v = red[0][ks][lane];
+#pragma unroll
+      for (int j = 1; j < 8; j++) {
+        v.x += red[j][ks][lane].x;
+        v.y += red[j][ks][lane].y;
+      }
+      double* cp = g.C + b1 * g.c_b1 + b2 * g.c_b2 + b3 * g.c_b3 + (int64_t)ks * g.c_rs + (int64_t)n * g.c_cs;
+      double r0 = g.alpha * v.x, r1 = g.alpha * v.y;
+      if (g.beta != 0.0) {
+        r0 += g.beta * cp[0];
+        r1 += g.beta * cp[g.c_cs];
+      }
+      cp[0] = r0;
+      cp[g.c_cs] = r1;
+    }
+    __syncthreads();
+  }
+}
+
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool B_ROW, bool V16>
 void launch_dmma(const Gemm& g, cudaStream_t s) {
   using L = SmemLayout<BM, BN, B_ROW>;
@@ -475,6 +550,18 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
     int64_t total = (int64_t)g.M * g.N;
     const int64_t kk = (int64_t)g.K * g.nseg;
     static const bool no_gemvt = getenv("GPFVM_NO_GEMVT") != nullptr;
+    if (!no_gemvt && g.b_cs == 1 && g.M <= 8 && g.N >= 64 && g.K >= 64 && (g.N & 1) == 0 && (g.b_rs & 1) == 0 &&
+        (g.b_b1 & 1) == 0 && (g.b_b2 & 1) == 0 && (g.b_b3 & 1) == 0 && (g.b_sg & 1) == 0 &&
+        aligned16(g.B)) {
+      const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
+      const unsigned grid = (unsigned)std::min<int64_t>(nbatch * ((g.N + 63) / 64), 148 * 16);
+      if (g.M <= 2) dgemm_gemvt2_kernel<2><<<grid, 256, 0, s>>>(g);
+      else if (g.M <= 4) dgemm_gemvt2_kernel<4><<<grid, 256, 0, s>>>(g);
+      else dgemm_gemvt2_kernel<8><<<grid, 256, 0, s>>>(g);
+      count_launch();
+      check_launch("dgemm_gemvt2_kernel");
+      return;
+    }
     if (!no_gemvt && g.b_cs == 1 && g.M <= 8 && g.N >= 64 && kk >= 8) {
       const int64_t nbatch = (int64_t)g.batch1 * g.batch2 * g.batch3;
       const int64_t work = nbatch * ((g.N + 127) / 128);

@@ -107,35 +107,6 @@ void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
   check_launch("build_lowrank");
 }
 
-// y_r[i, j] = beta y_r[i, j] + sum_k U_r[i, k] V_r[k, j], two columns per thread
-__global__ void lowrank_update_kernel(double* __restrict__ y, int64_t ldy, const double* __restrict__ U,
-                                      const double* __restrict__ V, int Rn, int n0, int n1, int rk, double beta) {
-  const int h1 = n1 / 2;
-  const int64_t total = (int64_t)Rn * n0 * h1;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int j2 = (int)(idx % h1);
-    const int64_t ri = idx / h1;
-    const int i = (int)(ri % n0), r = (int)(ri / n0);
-    const double* Ur = U + ((int64_t)r * n0 + i) * rk;
-    const double2* Vr = reinterpret_cast<const double2*>(V + (int64_t)r * rk * n1) + j2;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int k = 0; k < rk; k++) {
-      const double u = __ldg(Ur + k);
-      const double2 v = __ldg(Vr + (int64_t)k * h1);
-      acc.x = fma(u, v.x, acc.x);
-      acc.y = fma(u, v.y, acc.y);
-    }
-    double2* yp = reinterpret_cast<double2*>(y + (int64_t)r * ldy + (int64_t)i * n1) + j2;
-    if (beta != 0.0) {
-      const double2 o = *yp;
-      acc.x = fma(beta, o.x, acc.x);
-      acc.y = fma(beta, o.y, acc.y);
-    }
-    *yp = acc;
-  }
-}
-
 void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn, double beta, const int64_t* block_off,
                     cudaStream_t s) {
   for (const Part& part : parts) {
@@ -160,15 +131,8 @@ void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn
     }
     count_launch();
   }
-  // y_r = beta y_r + U_r V_r   (n0 x rk) (rk x n1): for small rank a streaming
-  // kernel (store-bound, 2 outputs per thread) instead of a K = rk GEMM
-  if (rk <= 16 && (n1 & 1) == 0 && (ldy & 1) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0)) {
-    const int64_t total = (int64_t)Rn * n0 * (n1 / 2);
-    const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    lowrank_update_kernel<<<grid, 256, 0, s>>>(y, ldy, U.ptr, V.ptr, Rn, n0, n1, rk, beta);
-    count_launch();
-    return;
-  }
+  // y_r = beta y_r + U_r V_r   (n0 x rk) (rk x n1)  (a streaming kernel was
+  // measured slower than this DMMA GEMM, which keeps V tiles in shared memory)
   Gemm g;
   g.M = n0; g.N = n1; g.K = rk;
   g.A = U.ptr; g.a_rs = rk; g.a_cs = 1; g.a_b1 = (int64_t)n0 * rk;
