@@ -49,13 +49,126 @@ __global__ void scaled_copy2(double* dst, const double* __restrict__ src, double
 }
 }  // namespace
 
-// Mark and build the low-rank parts of every 2D output block.
+// y[r][a][i][b] = beta y[r][a][i][b] + sum_p U[i][p] W[r][p][a][b]   (P <= 16);
+// b fastest across threads (coalesced y and W), U broadcast.
+__global__ void mode_update_kernel(double* __restrict__ y, int64_t ldy, const double* __restrict__ U,
+                                   const double* __restrict__ W, int R, int A, int ns, int B, int P, double beta) {
+  const int64_t per = (int64_t)A * ns * B;
+  const int64_t total = per * R;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / per;
+    const int64_t e = idx - r * per;
+    const int64_t ai = e / B;
+    const int b = (int)(e - ai * B);
+    const int a = (int)(ai / ns), i = (int)(ai - (int64_t)a * ns);
+    const double* Wr = W + (int64_t)r * P * A * B + (int64_t)a * B + b;
+    const double* Ui = U + (int64_t)i * P;
+    double acc = 0.0;
+    for (int q = 0; q < P; q++) acc = fma(__ldg(Ui + q), __ldg(Wr + (int64_t)q * A * B), acc);
+    double* yp = y + r * ldy + e;
+    *yp = (beta != 0.0) ? fma(beta, *yp, acc) : acc;
+  }
+}
+
+int64_t ModeUpdate::workspace_per_rhs() const {
+  int64_t w = 0;
+  for (const auto& part : parts)
+    for (const auto& k : part.ks) w = std::max(w, k.workspace_per_rhs());
+  return w;
+}
+
+void ModeUpdate::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta,
+                       const int64_t* block_off, double* w0, double* w1, cudaStream_t st) const {
+  const int64_t AB = (int64_t)A * B;
+  for (const auto& part : parts)
+    for (size_t q = 0; q < part.ks.size(); q++)
+      part.ks[q].apply(x + block_off[part.J], ldx, W.ptr + (part.p0 + (int64_t)q) * AB, (int64_t)P * AB, R, 0.0, w0,
+                       w1, st);
+  const int64_t total = (int64_t)R * A * ns * B;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
+  mode_update_kernel<<<grid, 256, 0, st>>>(y, ldy, U.ptr, W.ptr, R, A, ns, B, P, beta);
+  count_launch();
+}
+
+// Mode updates of every d >= 3 output block (see ModeUpdate in problem.h).
+static void build_modes(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
+  const int nb = (int)p->blocks.size(), d = p->ndim;
+  pl.modes.clear();
+  pl.modes.resize(nb);
+  if (d < 3 || getenv("GPFVM_NO_MODEUPDATE")) return;
+  for (int I = 0; I < nb; I++) {
+    const BlockInt& BI = p->blocks[I];
+    for (int k : pl.by_out[I]) {
+      PairOp& op = pl.pairs[k];
+      if (op.J == I) continue;
+      const BlockInt& BJ = p->blocks[op.J];
+      int sdim = -1, nsing = 0;
+      for (int i = 0; i < d; i++)
+        if (BJ.shape[i] == 1 && BI.shape[i] > 1) { sdim = i; nsing++; }
+      if (nsing != 1) continue;
+      std::vector<const KronTerm*> ts;
+      for (const auto& t : p->terms)
+        if (t.I == I && t.J == op.J) ts.push_back(&t);
+      if (ts.empty()) continue;
+      // find / create the mode-s update of this output block
+      ModeUpdate* mu = nullptr;
+      for (auto& m : pl.modes[I])
+        if (m.s == sdim) mu = &m;
+      if (!mu) {
+        pl.modes[I].emplace_back();
+        mu = &pl.modes[I].back();
+        mu->s = sdim;
+        mu->A = 1; mu->B = 1;
+        for (int i = 0; i < sdim; i++) mu->A *= BI.shape[i];
+        for (int i = sdim + 1; i < d; i++) mu->B *= BI.shape[i];
+        mu->ns = BI.shape[sdim];
+      }
+      if (mu->P + (int)ts.size() > 16) continue;  // kernel bound: keep the plain pair
+      ModeUpdate::Part part;
+      part.J = op.J;
+      part.p0 = mu->P;
+      int in_r[GPFVM_MAX_DIMS], out_r[GPFVM_MAX_DIMS], dr = 0;
+      for (int i = 0; i < d; i++)
+        if (i != sdim) { in_r[dr] = BJ.shape[i]; out_r[dr] = BI.shape[i]; dr++; }
+      for (const KronTerm* t : ts) {
+        std::vector<std::vector<const double*>> fs(1);
+        for (int i = 0; i < d; i++)
+          if (i != sdim) fs[0].push_back(p->factors[t->fid[i]].data.ptr);
+        part.ks.emplace_back();
+        part.ks.back().build(dr, in_r, out_r, {1.0}, fs, s);
+      }
+      mu->P += (int)ts.size();
+      mu->parts.push_back(std::move(part));
+      op.lowrank = true;  // served by the mode update, skipped as a plain pair
+    }
+    // fixed columns U[:, p] = c_p F_s^p[:, 0]
+    for (auto& m : pl.modes[I]) {
+      m.U.ensure((size_t)m.ns * std::max(1, m.P));
+      for (const auto& part : m.parts) {
+        int q = 0;
+        for (const auto& t : p->terms) {
+          if (t.I != I || t.J != part.J) continue;
+          set_col_kernel<<<gb(m.ns), 256, 0, s>>>(m.U.ptr, m.P, part.p0 + q, p->factors[t.fid[m.s]].data.ptr, m.ns,
+                                                  t.coef);
+          count_launch();
+          q++;
+        }
+      }
+    }
+  }
+  check_launch("build_modes");
+}
+
+// Mark and build the low-rank parts of every 2D output block (and the mode
+// updates of d >= 3 output blocks).
 void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
   const int nb = (int)p->blocks.size();
   pl.lowrank.clear();
   pl.lowrank.resize(nb);
   pl.block_off.resize(nb);
   for (int b = 0; b < nb; b++) pl.block_off[b] = p->blocks[b].offset;
+  build_modes(p, pl, s);
   if (p->ndim != 2 || getenv("GPFVM_NO_LOWRANK")) return;
   for (int I = 0; I < nb; I++) {
     LowRank& lr = pl.lowrank[I];

@@ -260,6 +260,21 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
   plan->w0.resize(nb);
   plan->w1.resize(nb);
   build_lowrank(p, *plan, s);
+  // executed flops per right-hand side: plain pairs + low-rank / mode updates
+  plan->flops_per_rhs = 0.0;
+  for (const auto& op : plan->pairs)
+    if (!op.lowrank) plan->flops_per_rhs += op.ks.flops_per_rhs();
+  for (const auto& lr : plan->lowrank) {
+    for (const auto& part : lr.parts)
+      plan->flops_per_rhs += 2.0 * part.nin * part.P * (part.type == 0 ? lr.n1 : lr.n0);
+    plan->flops_per_rhs += 2.0 * lr.n0 * lr.n1 * lr.rk;
+  }
+  for (const auto& ms : plan->modes)
+    for (const auto& mu : ms) {
+      for (const auto& part : mu.parts)
+        for (const auto& k : part.ks) plan->flops_per_rhs += k.flops_per_rhs();
+      plan->flops_per_rhs += 2.0 * mu.A * mu.ns * mu.B * mu.P;
+    }
   p->plan = std::move(plan);
 }
 
@@ -272,6 +287,11 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
   LowRank& lr = pl.lowrank[I];
   if (lr.rk > 0) {
     lr.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), s);
+    overwrite = false;
+  }
+  for (const auto& mu : pl.modes[I]) {
+    if (mu.P == 0) continue;
+    mu.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), pl.w0[I].ptr, pl.w1[I].ptr, s);
     overwrite = false;
   }
   for (int k : pl.by_out[I]) {
@@ -288,6 +308,14 @@ static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
   for (size_t I = 0; I < pl.by_out.size(); I++) {
     int64_t need = 0;
     for (int k : pl.by_out[I]) need = std::max(need, pl.pairs[k].ks.workspace_per_rhs());
+    for (auto& mu : pl.modes[I]) {
+      need = std::max(need, mu.workspace_per_rhs());
+      const size_t nw = (size_t)nrhs * std::max(1, mu.P) * mu.A * mu.B;
+      if (mu.W.n < nw) {
+        pl.release_graphs();
+        mu.W.ensure(nw);
+      }
+    }
     size_t n = (size_t)std::max<int64_t>(1, need * nrhs);
     if (pl.w0[I].n < n) {
       pl.release_graphs();  // captured graphs reference the old buffers

@@ -112,12 +112,34 @@ struct LowRank {
              cudaStream_t s);
 };
 
+// d >= 3 output block: couplings from blocks that are singleton in exactly one
+// dimension s (IC planes, boundary faces) are mode-s updates
+//   y[a, i, b] += sum_p U[i, p] W_p[a, b],   W_p = (x)_{k != s} F_k^p x_J,
+// U[:, p] = c_p F_s^p[:, 0] (fixed).  The W_p are (d-1)-dimensional Kronecker
+// products on the small input block (one single-term KronSum each); the update
+// is one streaming pass over y instead of full-size mode products that expand
+// the singleton dimension.
+struct ModeUpdate {
+  struct Part {
+    int J = 0, p0 = 0;
+    std::vector<KronSum> ks;  // one per term
+  };
+  int s = 0, A = 1, ns = 1, B = 1, P = 0;
+  DevBuf U;    // [ns][P]
+  DevBuf W;    // [R][P][A][B]
+  std::vector<Part> parts;
+  int64_t workspace_per_rhs() const;
+  void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, const int64_t* block_off,
+             double* w0, double* w1, cudaStream_t s) const;
+};
+
 // Matvec plan: one KronSum per nonzero block pair, grouped by output block
 // (graph branches), with CUDA-graph replay cached per (x, y, nrhs, ld).
 struct MatvecPlan {
   std::vector<PairOp> pairs;
   std::vector<std::vector<int>> by_out;
   std::vector<LowRank> lowrank;  // per output block (rk = 0: unused)
+  std::vector<std::vector<ModeUpdate>> modes;  // per output block (d >= 3)
   std::vector<int64_t> block_off;
   std::vector<DevBuf> w0, w1;  // per output-block branch
   std::vector<cudaStream_t> branch;
