@@ -49,25 +49,24 @@ __global__ void scaled_copy2(double* dst, const double* __restrict__ src, double
 }
 }  // namespace
 
-// y[r][a][i][b] = beta y[r][a][i][b] + sum_p U[i][p] W[r][p][a][b]   (P <= 16);
-// b fastest across threads (coalesced y and W), U broadcast.
+// y[r][a][i][b] = beta y[r][a][i][b] + sum_p U[i][p] W[r][p][a][b]   (P <= 16).
+// blockIdx.y walks the (r, a) slabs (each ns*B contiguous doubles of y), the
+// x-dimension the slab: coalesced y and W, U broadcast, 32-bit index math.
 __global__ void mode_update_kernel(double* __restrict__ y, int64_t ldy, const double* __restrict__ U,
                                    const double* __restrict__ W, int R, int A, int ns, int B, int P, double beta) {
-  const int64_t per = (int64_t)A * ns * B;
-  const int64_t total = per * R;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / per;
-    const int64_t e = idx - r * per;
-    const int64_t ai = e / B;
-    const int b = (int)(e - ai * B);
-    const int a = (int)(ai / ns), i = (int)(ai - (int64_t)a * ns);
-    const double* Wr = W + (int64_t)r * P * A * B + (int64_t)a * B + b;
-    const double* Ui = U + (int64_t)i * P;
-    double acc = 0.0;
-    for (int q = 0; q < P; q++) acc = fma(__ldg(Ui + q), __ldg(Wr + (int64_t)q * A * B), acc);
-    double* yp = y + r * ldy + e;
-    *yp = (beta != 0.0) ? fma(beta, *yp, acc) : acc;
+  const int slab = ns * B;
+  const int64_t AB = (int64_t)A * B;
+  for (int ra = blockIdx.y; ra < R * A; ra += gridDim.y) {
+    const int r = ra / A, a = ra - r * A;
+    double* yr = y + (int64_t)r * ldy + (int64_t)a * slab;
+    const double* Wr = W + (int64_t)r * P * AB + (int64_t)a * B;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < slab; e += gridDim.x * blockDim.x) {
+      const int i = e / B, b = e - i * B;
+      const double* Ui = U + (int64_t)i * P;
+      double acc = 0.0;
+      for (int q = 0; q < P; q++) acc = fma(__ldg(Ui + q), __ldg(Wr + (int64_t)q * AB + b), acc);
+      yr[e] = (beta != 0.0) ? fma(beta, yr[e], acc) : acc;
+    }
   }
 }
 
@@ -85,9 +84,14 @@ void ModeUpdate::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int
     for (size_t q = 0; q < part.ks.size(); q++)
       part.ks[q].apply(x + block_off[part.J], ldx, W.ptr + (part.p0 + (int64_t)q) * AB, (int64_t)P * AB, R, 0.0, w0,
                        w1, st);
-  const int64_t total = (int64_t)R * A * ns * B;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 16));
-  mode_update_kernel<<<grid, 256, 0, st>>>(y, ldy, U.ptr, W.ptr, R, A, ns, B, P, beta);
+  const int slab = ns * B;
+  const int bx = slab >= 256 ? 256 : 128;
+  // ~16 CTAs per SM in total, split between slab chunks (x) and slabs (y)
+  const int64_t nslab = (int64_t)R * A;
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((slab + bx - 1) / bx, (148 * 16 + nslab - 1) / nslab));
+  const int64_t gy = std::min<int64_t>(nslab, std::max<int64_t>(1, 148 * 16 / gx));
+  mode_update_kernel<<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(gy, 65535)), bx, 0, st>>>(y, ldy, U.ptr, W.ptr,
+                                                                                                 R, A, ns, B, P, beta);
   count_launch();
 }
 
