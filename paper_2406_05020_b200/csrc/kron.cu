@@ -15,6 +15,9 @@
 // (the p-sum is the K-concatenation of the last contraction).  d = 1: a single
 // K-segment GEMM  Y_r = sum_p X_r (c_p F^p)^T.  Coefficients are folded into
 // the first-applied factor.
+#include <algorithm>
+#include <cstdlib>
+
 #include "problem.h"
 
 namespace gpfvm {
@@ -92,17 +95,44 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
     return;
   }
   if (d == 3 && !rev) {
-    // 3D forward plain layout: stk0 rows interleaved (j0,p) with c_p, stk1 P plain blocks,
-    // stk2 columns concatenated (p,k2)
-    for (int i = 0; i < 3; i++) stk[i].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[i] * nin[i] * P));
+    // 3D forward plain layout: stk0 rows interleaved (j0,q) over the Q0 distinct
+    // dim-0 factors, stk1 P plain blocks with c_p, stk2 columns concatenated
+    // (q,k2) over the Q2 distinct dim-2 factors.  Terms sharing a factor share
+    // its stage-0 slice / stage-2 K-segment (e.g. the 6 wave-operator term pairs
+    // use 3 time and 3 y factors: stage 0 and stage 2 flops halve).  Dedup only
+    // where the middle stage runs per term (the layout it needs).
+    const bool per_term = P > 1 && nout[1] >= 64 && nin[2] >= 32 && !getenv("GPFVM_NO_DEDUP");
+    u0.assign(P, 0);
+    u2.assign(P, 0);
+    std::vector<const double*> d0, d2;
     for (int p = 0; p < P; p++) {
-      restack_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr, factors[p][0], coefs[p], p, P,
-                                                                     nout[0], nin[0], 0);
+      int q0 = per_term ? (int)(std::find(d0.begin(), d0.end(), factors[p][0]) - d0.begin()) : (int)d0.size();
+      if (q0 == (int)d0.size()) d0.push_back(factors[p][0]);
+      int q2 = per_term ? (int)(std::find(d2.begin(), d2.end(), factors[p][2]) - d2.begin()) : (int)d2.size();
+      if (q2 == (int)d2.size()) d2.push_back(factors[p][2]);
+      u0[p] = q0;
+      u2[p] = q2;
+    }
+    Q0 = (int)d0.size();
+    Q2 = (int)d2.size();
+    // without dedup the coefficient stays on the dim-0 factor (identity maps)
+    stk[0].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[0] * nin[0] * Q0));
+    stk[1].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[1] * nin[1] * P));
+    stk[2].ensure((size_t)std::max<int64_t>(1, (int64_t)nout[2] * nin[2] * Q2));
+    for (int q = 0; q < Q0; q++) {
+      restack_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr, d0[q], per_term ? 1.0 : coefs[q], q,
+                                                                     Q0, nout[0], nin[0], 0);
+      count_launch();
+    }
+    for (int p = 0; p < P; p++) {
       scaled_copy_kernel<<<gsz((int64_t)nout[1] * nin[1]), 256, 0, s>>>(stk[1].ptr + (int64_t)p * nout[1] * nin[1],
-                                                                         factors[p][1], 1.0, (int64_t)nout[1] * nin[1]);
-      restack_kernel<<<gsz((int64_t)nout[2] * nin[2]), 256, 0, s>>>(stk[2].ptr, factors[p][2], 1.0, p, P, nout[2],
-                                                                     nin[2], 1);
-      count_launch(3);
+                                                                         factors[p][1], per_term ? coefs[p] : 1.0,
+                                                                         (int64_t)nout[1] * nin[1]);
+      count_launch();
+    }
+    for (int q = 0; q < Q2; q++) {
+      restack_kernel<<<gsz((int64_t)nout[2] * nin[2]), 256, 0, s>>>(stk[2].ptr, d2[q], 1.0, q, Q2, nout[2], nin[2], 1);
+      count_launch();
     }
     check_launch("KronSum::build (3D)");
     return;
@@ -135,6 +165,9 @@ int64_t KronSum::workspace_per_rhs() const {
 
 double KronSum::flops_per_rhs() const {
   if (P == 0) return 0.0;
+  if (d == 3 && !rev && Q0 > 0)
+    return 2.0 * ((double)Q0 * nout[0] * nin[0] * nin[1] * nin[2] + (double)P * nout[0] * nout[1] * nin[1] * nin[2] +
+                  (double)Q2 * nout[0] * nout[1] * nout[2] * nin[2]);
   return order_flops(d, P, nin, nout, rev);
 }
 
@@ -193,11 +226,13 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
   }
   if (d == 3 && !rev) {
     const int64_t n0 = nout[0], n1 = nout[1], n2 = nout[2], m0 = nin[0], m1 = nin[1], m2 = nin[2];
-    const int64_t z0 = (int64_t)P * n0 * m1 * m2;  // [r][(j0,p)][k1][k2]
-    const int64_t z1 = n0 * n1 * P * m2;           // [r][j0][j1][p][k2]
+    const bool per_term = P > 1 && n1 >= 64 && m2 >= 32 && Q0 > 0;
+    const int64_t q0 = per_term ? Q0 : P, q2 = per_term ? Q2 : P;
+    const int64_t z0 = q0 * n0 * m1 * m2;  // [r][(j0,q0)][k1][k2]
+    const int64_t z1 = n0 * n1 * q2 * m2;  // [r][j0][j1][q2][k2]
     Gemm g0, g1, g2;
-    // stage 0: Z0_r[(j0,p)][(k1,k2)] = sum_k0 c_p F0^p[j0][k0] X_r[k0][(k1,k2)]
-    g0.M = (int)(P * n0); g0.N = (int)(m1 * m2); g0.K = (int)m0;
+    // stage 0: Z0_r[(j0,q)][(k1,k2)] = sum_k0 F0^q[j0][k0] X_r[k0][(k1,k2)]
+    g0.M = (int)(q0 * n0); g0.N = (int)(m1 * m2); g0.K = (int)m0;
     g0.A = stk[0].ptr; g0.a_rs = m0; g0.a_cs = 1;
     g0.B = x; g0.b_rs = m1 * m2; g0.b_cs = 1; g0.b_b1 = ldx;
     g0.C = w0; g0.c_rs = m1 * m2; g0.c_cs = 1; g0.c_b1 = z0;
@@ -211,24 +246,28 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     g1.C = w1; g1.c_rs = (int64_t)P * m2; g1.c_cs = 1;
     g1.c_b1 = n1 * P * m2; g1.c_b2 = m2; g1.c_b3 = z1;
     g1.batch1 = (int)n0; g1.batch2 = P; g1.batch3 = R;
-    if (P > 1 && n1 >= 64 && m2 >= 32) {
+    if (per_term) {
       // one plain batched GEMM per term over the combined (r, j0) batch (uniform
-      // strides) so the tensor-op template applies
+      // strides) so the tensor-op template applies; terms with the same dim-2
+      // factor accumulate into the same K-segment
+      std::vector<char> seen(q2, 0);
       for (int p = 0; p < P; p++) {
         Gemm gp = g1;
         gp.A = stk[1].ptr + (int64_t)p * n1 * m1; gp.a_b2 = 0;
-        gp.B = w0 + (int64_t)p * m1 * m2; gp.b_b1 = (int64_t)P * m1 * m2; gp.b_b2 = gp.b_b3 = 0;
-        gp.C = w1 + (int64_t)p * m2; gp.c_b1 = n1 * P * m2; gp.c_b2 = gp.c_b3 = 0;
+        gp.B = w0 + (int64_t)u0[p] * m1 * m2; gp.b_b1 = q0 * m1 * m2; gp.b_b2 = gp.b_b3 = 0;
+        gp.C = w1 + (int64_t)u2[p] * m2; gp.c_rs = q2 * m2; gp.c_b1 = n1 * q2 * m2; gp.c_b2 = gp.c_b3 = 0;
         gp.batch1 = (int)(n0 * R); gp.batch2 = gp.batch3 = 1;
+        gp.beta = seen[u2[p]] ? 1.0 : 0.0;
+        seen[u2[p]] = 1;
         run_gemm(gp, s);
       }
     } else {
       run_gemm(g1, s);
     }
-    // stage 2: Y_r[(j0,j1)][j2] = sum_(p,k2) Z1_r[(j0,j1)][(p,k2)] F2^p[j2][k2]
-    g2.M = (int)(n0 * n1); g2.N = (int)n2; g2.K = (int)(P * m2);
-    g2.A = w1; g2.a_rs = (int64_t)P * m2; g2.a_cs = 1; g2.a_b1 = z1;
-    g2.B = stk[2].ptr; g2.b_rs = 1; g2.b_cs = (int64_t)P * m2;
+    // stage 2: Y_r[(j0,j1)][j2] = sum_(q,k2) Z1_r[(j0,j1)][(q,k2)] F2^q[j2][k2]
+    g2.M = (int)(n0 * n1); g2.N = (int)n2; g2.K = (int)(q2 * m2);
+    g2.A = w1; g2.a_rs = q2 * m2; g2.a_cs = 1; g2.a_b1 = z1;
+    g2.B = stk[2].ptr; g2.b_rs = 1; g2.b_cs = q2 * m2;
     g2.C = y; g2.c_rs = n2; g2.c_cs = 1; g2.c_b1 = ldy;
     g2.batch1 = R;
     g2.beta = beta;
