@@ -50,6 +50,13 @@ __global__ void coldot_sub_kernel(double* var, const double* __restrict__ Z, con
   }
 }
 
+// X[r][k] *= d[k] for r = blockIdx.y (rows of length n)
+__global__ void scale_rows_by_kernel(double* X, const double* __restrict__ d, int64_t n) {
+  double* xr = X + (int64_t)blockIdx.y * n;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    xr[k] *= d[k];
+}
+
 unsigned gs(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)); }
 
 }  // namespace
@@ -211,6 +218,50 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
   // through the cross-covariance Kronecker sums, then column sums of squares.
   if (pc.nb == 0) return;
   const int nb = (int)pc.nb;
+  if (pc.structured) {
+    // K_{*P} Y L^{-T} = K_{*P} (V (x) W) D^{-1} Z L^{-T} = Khat M with
+    // Khat = sum_a c_a (A_a V) (x) (B_a W) (the Ah, Bh above) and the nb rows of
+    // M = D^{-1} (sum_J Z_J L^{-T}[J rows, :]) cached per preconditioner.
+    if (!pc.LYT.ptr) {
+      pc.LYT.ensure((size_t)nb * pc.Np);
+      DevBuf w0, w1;
+      for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+        const int64_t wsz = std::max<int64_t>(1, pc.rot_ks[jb].workspace_per_rhs()) * nb;
+        w0.ensure((size_t)wsz);
+        w1.ensure((size_t)wsz);
+        pc.rot_ks[jb].apply(pc.Linv.ptr + pc.boff[jb], nb, pc.LYT.ptr, pc.Np, nb, jb == 0 ? 0.0 : 1.0, w0.ptr, w1.ptr,
+                            s);
+      }
+      scale_rows_by_kernel<<<dim3(gs(pc.Np), nb), 256, 0, s>>>(pc.LYT.ptr, pc.Dinv.ptr, pc.Np);
+      count_launch();
+      GPFVM_CUDA(cudaStreamSynchronize(s));
+    }
+    DevBuf Z;
+    Z.ensure((size_t)nb * ng);
+    bool first = true;
+    for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+      const int J = pc.bblocks[jb];
+      if (cp.terms[J].empty()) continue;
+      cross_apply(p, cp, J, 1.0, pc.Linv.ptr + pc.boff[jb], nb, Z.ptr, ng, nb, first ? 0.0 : 1.0, s);
+      first = false;
+    }
+    std::vector<double> coefs;
+    std::vector<std::vector<const double*>> fs;
+    for (size_t a = 0; a < tP.size(); a++) {
+      coefs.push_back(-tP[a].coef);
+      fs.push_back({Ah[a].ptr, Bh[a].ptr});
+    }
+    KronSum ks;
+    ks.build(p->ndim, p->blocks[pc.P].shape, cp.gshape, coefs, fs, s);
+    size_t need = (size_t)std::max<int64_t>(1, ks.workspace_per_rhs() * nb);
+    cp.w0.ensure(need);
+    cp.w1.ensure(need);
+    ks.apply(pc.LYT.ptr, pc.Np, Z.ptr, ng, nb, first ? 0.0 : 1.0, cp.w0.ptr, cp.w1.ptr, s);
+    coldot_sub_kernel<<<gs(ng), 256, 0, s>>>(var, Z.ptr, Z.ptr, nb, ng);
+    count_launch();
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
   if (!pc.LYT.ptr) {
     // L^{-1} Y^T with L^{-1} lower triangular: row panels touch only the
     // nonzero columns

@@ -73,7 +73,19 @@ struct Precond {
   std::vector<int64_t> boff;  // offset of each deflated block inside the b-vector
   int64_t nb = 0;
   DevBuf YT, Sinv, Linv;           // Y^T = (FD G_pb)^T (nb x Np), explicit S^{-1} = L^{-T} L^{-1}
-  DevBuf LYT;                      // L^{-1} Y^T (nb x Np), built on the first PRECOND predict
+  DevBuf LYT;                      // L^{-1} Y^T (nb x Np), built on the first PRECOND predict (dense path)
+  // Rotated couplings Z_J = (V (x) W)^T G_{P,J} = sum_s c_s (V^T F0_s) (x) (W^T F1_s)
+  // per deflated block.  structured: every deflated block is
+  // thin (IC-like m0 = 1 or BC-like m1 = 1), Y is never formed.
+  struct RotTerm {
+    double c = 0.0;
+    int m0 = 0, m1 = 0;
+    DevBuf R0, R1, LT;  // R0 = V^T F0 (n0 x m0), R1 = W^T F1 (n1 x m1), LT = long factor transposed
+  };
+  std::vector<std::vector<RotTerm>> rot;
+  std::vector<KronSum> rot_ks;
+  bool structured = false;
+  DevBuf yb, WT, DinvT;
   std::vector<KronSum> ks_bp;      // G_{I,P} per deflated block I (Kronecker sums)
   DevBuf kw0, kw1;                 // their workspaces (one vector)
   double shift = 0.0;

@@ -71,6 +71,17 @@ __global__ void sub_kernel(double* a, const double* __restrict__ b, int64_t n) {
   if (i < n) a[i] -= b[i];
 }
 
+// X[i][c] = v[i] * M[i][c]  (rows x cols)
+__global__ void row_scale_kernel(double* X, const double* __restrict__ v, const double* __restrict__ M, int rows,
+                                 int cols) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    X[k] = v[k / cols] * M[k];
+}
+__global__ void vec_mul_kernel(double* z, const double* __restrict__ a, const double* __restrict__ b, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) z[i] = a[i] * b[i];
+}
+
 __global__ void symm_kernel(double* A, int n) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -219,6 +230,152 @@ static void build_fd(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   GPFVM_CUDA(cudaStreamSynchronize(s));
 }
 
+// Rotated couplings Z_J (see Precond::RotTerm) and their Kronecker sums.
+static void build_rot(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
+  const int n0 = pc.n0, n1 = pc.n1;
+  pc.WT.ensure((size_t)n1 * n1);
+  transpose(pc.W.ptr, pc.WT.ptr, n1, n1, s);
+  pc.rot.clear();
+  pc.rot.resize(pc.bblocks.size());
+  pc.rot_ks.clear();
+  pc.rot_ks.resize(pc.bblocks.size());
+  pc.structured = getenv("GPFVM_LDL_DENSE") == nullptr;
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+    const int J = pc.bblocks[jb];
+    const BlockInt& BJ = p->blocks[J];
+    const bool ic = BJ.shape[0] == 1, bc = !ic && BJ.shape[1] == 1;
+    if (!ic && !bc) pc.structured = false;
+    std::vector<double> coefs;
+    std::vector<std::vector<const double*>> fs;
+    for (const auto& t : p->terms) {
+      if (t.I != pc.P || t.J != J) continue;
+      const Factor& F0 = p->factors[t.fid[0]];
+      const Factor& F1 = p->factors[t.fid[1]];
+      Precond::RotTerm rt;
+      rt.c = t.coef;
+      rt.m0 = F0.cols;
+      rt.m1 = F1.cols;
+      rt.R0.ensure((size_t)n0 * rt.m0);
+      rt.R1.ensure((size_t)n1 * rt.m1);
+      Gemm g;  // R0 = V^T F0
+      g.M = n0; g.N = rt.m0; g.K = n0;
+      g.A = pc.Vt.ptr; g.a_rs = n0; g.a_cs = 1;
+      g.B = F0.data.ptr; g.b_rs = rt.m0; g.b_cs = 1;
+      g.C = rt.R0.ptr; g.c_rs = rt.m0; g.c_cs = 1;
+      run_gemm(g, s);
+      g = Gemm();  // R1 = W^T F1
+      g.M = n1; g.N = rt.m1; g.K = n1;
+      g.A = pc.WT.ptr; g.a_rs = n1; g.a_cs = 1;
+      g.B = F1.data.ptr; g.b_rs = rt.m1; g.b_cs = 1;
+      g.C = rt.R1.ptr; g.c_rs = rt.m1; g.c_cs = 1;
+      run_gemm(g, s);
+      if (ic || bc) {  // transposed long factor: IC-like R1 (n1 x nJ), BC-like R0 (n0 x nJ)
+        const int rows = ic ? n1 : n0, cols = ic ? rt.m1 : rt.m0;
+        rt.LT.ensure((size_t)rows * cols);
+        transpose(ic ? rt.R1.ptr : rt.R0.ptr, rt.LT.ptr, rows, cols, s);
+      }
+      coefs.push_back(t.coef);
+      fs.push_back({rt.R0.ptr, rt.R1.ptr});
+      pc.rot[jb].push_back(std::move(rt));
+    }
+    pc.rot_ks[jb].build(p->ndim, BJ.shape, p->blocks[pc.P].shape, coefs, fs, s);
+  }
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+}
+
+// S -= Z^T D^{-1} Z block by block from the rotated thin factors (no Y): for
+// IC-like J (a = R0 column, L = R1) and BC-like J (b = R1 column, L = R0)
+//   IC-IC  L^T diag(D^{-T}(a o a')) L'          BC-BC  L^T diag(D^{-1}(b o b')) L'
+//   IC-BC  L^T diag(b') D^{-T} diag(a) L'       BC-IC  L^T diag(a') D^{-1} diag(b) L'
+// (all n x n x nJ GEMMs, ~1e3 x fewer flops than S = G_bb - G_pb^T Y).
+static void structured_schur(gpfvm_problem* p, Precond& pc, double* S, cudaStream_t s) {
+  const int n0 = pc.n0, n1 = pc.n1, nb = (int)pc.nb;
+  pc.DinvT.ensure((size_t)n1 * n0);
+  transpose(pc.Dinv.ptr, pc.DinvT.ptr, n0, n1, s);
+  DevBuf v, e, Mx, T;
+  const int nmax = std::max(n0, n1);
+  v.ensure(nmax);
+  e.ensure(nmax);
+  int64_t big = 0;
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++) big = std::max<int64_t>(big, p->blocks[pc.bblocks[jb]].size);
+  Mx.ensure((size_t)nmax * big);
+  T.ensure((size_t)nmax * big);
+  for (size_t jb = 0; jb < pc.bblocks.size(); jb++)
+    for (size_t kb = 0; kb < pc.bblocks.size(); kb++) {
+      const bool icJ = p->blocks[pc.bblocks[jb]].shape[0] == 1, icK = p->blocks[pc.bblocks[kb]].shape[0] == 1;
+      const int nJ = (int)p->blocks[pc.bblocks[jb]].size, nK = (int)p->blocks[pc.bblocks[kb]].size;
+      for (const auto& ra : pc.rot[jb])
+        for (const auto& rb : pc.rot[kb]) {
+          const double w = -ra.c * rb.c;
+          int inner = 0;      // length of the contracted long dimension
+          const double* Tp = nullptr;
+          if (icJ && icK) {
+            // e = D^{-T} (a o a'), T = diag(e) L'
+            vec_mul_kernel<<<g1(n0), 256, 0, s>>>(v.ptr, ra.R0.ptr, rb.R0.ptr, n0);
+            count_launch();
+            Gemm g;
+            g.M = 1; g.N = n1; g.K = n0;
+            g.A = v.ptr; g.a_rs = n0; g.a_cs = 1;
+            g.B = pc.Dinv.ptr; g.b_rs = n1; g.b_cs = 1;
+            g.C = e.ptr; g.c_rs = n1; g.c_cs = 1;
+            run_gemm(g, s);
+            row_scale_kernel<<<g1((int64_t)n1 * nK), 256, 0, s>>>(T.ptr, e.ptr, rb.R1.ptr, n1, nK);
+            count_launch();
+            inner = n1;
+          } else if (!icJ && !icK) {
+            // f = D^{-1} (b o b'), T = diag(f) L'
+            vec_mul_kernel<<<g1(n1), 256, 0, s>>>(v.ptr, ra.R1.ptr, rb.R1.ptr, n1);
+            count_launch();
+            Gemm g;
+            g.M = 1; g.N = n0; g.K = n1;
+            g.A = v.ptr; g.a_rs = n1; g.a_cs = 1;
+            g.B = pc.DinvT.ptr; g.b_rs = n0; g.b_cs = 1;
+            g.C = e.ptr; g.c_rs = n0; g.c_cs = 1;
+            run_gemm(g, s);
+            row_scale_kernel<<<g1((int64_t)n0 * nK), 256, 0, s>>>(T.ptr, e.ptr, rb.R0.ptr, n0, nK);
+            count_launch();
+            inner = n0;
+          } else if (icJ && !icK) {
+            // Mx = D^{-T} diag(a) L'  (n1 x nK), T = diag(b') Mx
+            row_scale_kernel<<<g1((int64_t)n0 * nK), 256, 0, s>>>(T.ptr, ra.R0.ptr, rb.R0.ptr, n0, nK);
+            count_launch();
+            Gemm g;
+            g.M = n1; g.N = nK; g.K = n0;
+            g.A = pc.DinvT.ptr; g.a_rs = n0; g.a_cs = 1;
+            g.B = T.ptr; g.b_rs = nK; g.b_cs = 1;
+            g.C = Mx.ptr; g.c_rs = nK; g.c_cs = 1;
+            run_gemm(g, s);
+            row_scale_kernel<<<g1((int64_t)n1 * nK), 256, 0, s>>>(T.ptr, rb.R1.ptr, Mx.ptr, n1, nK);
+            count_launch();
+            inner = n1;
+          } else {
+            // My = D^{-1} diag(b) L'  (n0 x nK), T = diag(a') My
+            row_scale_kernel<<<g1((int64_t)n1 * nK), 256, 0, s>>>(T.ptr, ra.R1.ptr, rb.R1.ptr, n1, nK);
+            count_launch();
+            Gemm g;
+            g.M = n0; g.N = nK; g.K = n1;
+            g.A = pc.Dinv.ptr; g.a_rs = n1; g.a_cs = 1;
+            g.B = T.ptr; g.b_rs = nK; g.b_cs = 1;
+            g.C = Mx.ptr; g.c_rs = nK; g.c_cs = 1;
+            run_gemm(g, s);
+            row_scale_kernel<<<g1((int64_t)n0 * nK), 256, 0, s>>>(T.ptr, rb.R0.ptr, Mx.ptr, n0, nK);
+            count_launch();
+            inner = n0;
+          }
+          Tp = T.ptr;
+          // S[J rows][K cols] += w * LT_J (nJ x inner) T (inner x nK)
+          Gemm g;
+          g.M = nJ; g.N = nK; g.K = inner;
+          g.A = ra.LT.ptr; g.a_rs = inner; g.a_cs = 1;
+          g.B = Tp; g.b_rs = nK; g.b_cs = 1;
+          g.C = S + pc.boff[jb] * nb + pc.boff[kb]; g.c_rs = nb; g.c_cs = 1;
+          g.alpha = w; g.beta = 1.0;
+          run_gemm(g, s);
+        }
+    }
+  GPFVM_CUDA(cudaStreamSynchronize(s));
+}
+
 static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   const int nblk = (int)p->blocks.size();
   pc.nb = 0;
@@ -232,9 +389,10 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   GPFVM_CHECK(pc.nb <= 16384, GPFVM_ERR_UNSUPPORTED, "block-LDL: more than 16384 deflated observations");
   const int nb = (int)pc.nb;
   const int64_t np = pc.Np;
-  pc.YT.ensure((size_t)nb * np);
   DevBuf S, S0, eye, Lf;
   PhaseTimer pt(s);
+  build_rot(p, pc, s);
+  if (!pc.structured) pc.YT.ensure((size_t)nb * np);
   S.ensure((size_t)nb * nb);
   fill(S.ptr, 0.0, (int64_t)nb * nb, s);
   // identity right-hand sides per deflated block, pushed through the Kronecker terms
@@ -270,6 +428,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     count_launch();
     GPFVM_CUDA(cudaStreamSynchronize(s));
   }
+  if (!pc.structured) {
   // Y^T = FD(G_pb) rows without forming G_pb: per deflated block J,
   // (V (x) W)^T G_{P,J} = sum_tau c_tau (V^T F0_tau) (x) (W^T F1_tau) is again a
   // Kronecker sum with small factors, applied to the identity of block J; then
@@ -327,6 +486,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     GPFVM_CUDA(cudaStreamSynchronize(s));
   }
   pt.mark("ldl: Y = FD(Gpb)");
+  }  // !structured
   // G_{I,P} Kronecker sums (used by P^{-1})
   pc.ks_bp.clear();
   pc.ks_bp.resize(pc.bblocks.size());
@@ -346,9 +506,13 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
       pc.ks_bp[ib].build(p->ndim, p->blocks[pc.P].shape, p->blocks[I].shape, coefs, fs, s);
       wmax = std::max(wmax, pc.ks_bp[ib].workspace_per_rhs());
     }
+    for (const auto& k : pc.rot_ks) wmax = std::max(wmax, k.workspace_per_rhs());
     pc.kw0.ensure((size_t)wmax);
     pc.kw1.ensure((size_t)wmax);
   }
+  if (pc.structured) {
+    structured_schur(p, pc, S.ptr, s);
+  } else {
   // S = G_bb - G_bp Y: instead of the dense GEMM with G_pb^T (nb x nb x N_PDE
   // flops) apply each Kronecker sum -G_{I,P} to the nb columns of Y, contracted
   // in its cheapest mode order (IC/BC blocks are thin in one dimension: ~100x
@@ -377,6 +541,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     }
     GPFVM_CUDA(cudaStreamSynchronize(s));
   }
+  }  // structured / dense Schur
   symm_kernel<<<g1((int64_t)nb * nb), 256, 0, s>>>(S.ptr, nb);
   count_launch();
   pt.mark("ldl: S = Gbb - Gpb^T Y");
@@ -434,6 +599,7 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   pc.rb.ensure(nb);
   pc.zb.ensure(nb);
   pc.cvec.ensure(nb);
+  pc.yb.ensure((size_t)np);
   GPFVM_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -512,7 +678,17 @@ void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s)
     const BlockInt& B = p->blocks[pc.bblocks[jb]];
     copy(z + B.offset, pc.zb.ptr + pc.boff[jb], B.size, s);
   }
-  axpy_many(zp, pc.YT.ptr, pc.Np, pc.zb.ptr, -1.0, pc.Np, nb, s);  // z_p -= Y z_b
+  if (pc.structured) {
+    // z_p -= FD G_pb z_b = (V (x) W) D^{-1} sum_J Z_J z_b,J
+    for (size_t jb = 0; jb < pc.bblocks.size(); jb++)
+      pc.rot_ks[jb].apply(pc.zb.ptr + pc.boff[jb], p->blocks[pc.bblocks[jb]].size, pc.t2.ptr, pc.Np, 1,
+                          jb == 0 ? 0.0 : 1.0, pc.kw0.ptr, pc.kw1.ptr, s);
+    fd_backward(pc, pc.yb.ptr, pc.Np, 1, s);
+    sub_kernel<<<g1(pc.Np), 256, 0, s>>>(zp, pc.yb.ptr, pc.Np);
+    count_launch();
+  } else {
+    axpy_many(zp, pc.YT.ptr, pc.Np, pc.zb.ptr, -1.0, pc.Np, nb, s);  // z_p -= Y z_b
+  }
 }
 
 static void ensure_krylov(gpfvm_problem* p, int need, cudaStream_t s) {
