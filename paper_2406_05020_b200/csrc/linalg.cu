@@ -30,6 +30,7 @@ __global__ void potrf_diag_kernel(double* A, int n, int k, int kb, int* info) {
     s[r][c] = A[(int64_t)(k + r) * n + k + c];
   }
   __syncthreads();
+  __shared__ double inv_s;
   for (int j = 0; j < kb; j++) {
     if (t == 0) {
       double d = s[j][j];
@@ -37,11 +38,13 @@ __global__ void potrf_diag_kernel(double* A, int n, int k, int kb, int* info) {
         if (*info == 0) *info = k + j + 1;
         d = NAN;
       }
-      s[j][j] = sqrt(d);
+      const double r = rsqrt(d);  // one reciprocal square root instead of sqrt + divisions
+      s[j][j] = d * r;
+      inv_s = r;
     }
     __syncthreads();
-    double ljj = s[j][j];
-    for (int r = j + 1 + t; r < kb; r += blockDim.x) s[r][j] /= ljj;
+    const double inv = inv_s;
+    for (int r = j + 1 + t; r < kb; r += blockDim.x) s[r][j] *= inv;
     __syncthreads();
     // update trailing columns of the diagonal block
     for (int i = t; i < kb * kb; i += blockDim.x) {
@@ -59,21 +62,34 @@ __global__ void potrf_diag_kernel(double* A, int n, int k, int kb, int* info) {
 // rows r >= k+kb:  A[r, k:k+kb] <- A[r, k:k+kb] L11^{-T}
 __global__ void potrf_panel_kernel(double* A, int n, int k, int kb) {
   __shared__ double L[PB][PB + 1];
+  __shared__ double dinv[PB];
   for (int i = threadIdx.x; i < kb * kb; i += blockDim.x) {
     int r = i / kb, c = i % kb;
     L[r][c] = A[(int64_t)(k + r) * n + k + c];
   }
   __syncthreads();
+  if (threadIdx.x < kb) dinv[threadIdx.x] = 1.0 / L[threadIdx.x][threadIdx.x];
+  __syncthreads();
   int r = k + kb + blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   double x[PB];
   double* row = A + (int64_t)r * n + k;
-  for (int j = 0; j < kb; j++) {
-    double v = row[j];
-    for (int i = 0; i < j; i++) v -= x[i] * L[j][i];
-    x[j] = v / L[j][j];
+#pragma unroll
+  for (int j = 0; j < PB; j++)
+    if (j < kb) x[j] = row[j];
+#pragma unroll
+  for (int j = 0; j < PB; j++) {
+    if (j < kb) {
+      double v = x[j];
+#pragma unroll
+      for (int i = 0; i < PB; i++)
+        if (i < j) v -= x[i] * L[j][i];
+      x[j] = v * dinv[j];
+    }
   }
-  for (int j = 0; j < kb; j++) row[j] = x[j];
+#pragma unroll
+  for (int j = 0; j < PB; j++)
+    if (j < kb) row[j] = x[j];
 }
 
 // Forward substitution on a diagonal block: B[k:k+kb, c] <- L11^{-1} B[k:k+kb, c]
@@ -83,16 +99,29 @@ __global__ void trsm_lower_diag_kernel(const double* L, int n, double* B, int nr
     int r = i / kb, c = i % kb;
     s[r][c] = L[(int64_t)(k + r) * n + k + c];
   }
+  __shared__ double dinv[PB];
+  __syncthreads();
+  if (threadIdx.x < kb) dinv[threadIdx.x] = 1.0 / s[threadIdx.x][threadIdx.x];
   __syncthreads();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nrhs) return;
   double x[PB];
-  for (int i = 0; i < kb; i++) {
-    double v = B[(int64_t)(k + i) * nrhs + c];
-    for (int j = 0; j < i; j++) v -= s[i][j] * x[j];
-    x[i] = v / s[i][i];
-    B[(int64_t)(k + i) * nrhs + c] = x[i];
+#pragma unroll
+  for (int i = 0; i < PB; i++)
+    if (i < kb) x[i] = B[(int64_t)(k + i) * nrhs + c];
+#pragma unroll
+  for (int i = 0; i < PB; i++) {
+    if (i < kb) {
+      double v = x[i];
+#pragma unroll
+      for (int j = 0; j < PB; j++)
+        if (j < i) v -= s[i][j] * x[j];
+      x[i] = v * dinv[i];
+    }
   }
+#pragma unroll
+  for (int i = 0; i < PB; i++)
+    if (i < kb) B[(int64_t)(k + i) * nrhs + c] = x[i];
 }
 
 // Backward substitution with U = L^T (U upper, row-major): B[k:k+kb] <- U11^{-1} B[k:k+kb]
@@ -102,16 +131,30 @@ __global__ void trsm_upper_diag_kernel(const double* U, int n, double* B, int nr
     int r = i / kb, c = i % kb;
     s[r][c] = U[(int64_t)(k + r) * n + k + c];
   }
+  __shared__ double dinv[PB];
+  __syncthreads();
+  if (threadIdx.x < kb) dinv[threadIdx.x] = 1.0 / s[threadIdx.x][threadIdx.x];
   __syncthreads();
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nrhs) return;
+  // compile-time indices (guards on kb) keep x in registers
   double x[PB];
-  for (int i = kb - 1; i >= 0; i--) {
-    double v = B[(int64_t)(k + i) * nrhs + c];
-    for (int j = i + 1; j < kb; j++) v -= s[i][j] * x[j];
-    x[i] = v / s[i][i];
-    B[(int64_t)(k + i) * nrhs + c] = x[i];
+#pragma unroll
+  for (int i = 0; i < PB; i++)
+    if (i < kb) x[i] = B[(int64_t)(k + i) * nrhs + c];
+#pragma unroll
+  for (int i = PB - 1; i >= 0; i--) {
+    if (i < kb) {
+      double v = x[i];
+#pragma unroll
+      for (int j = 0; j < PB; j++)
+        if (j > i && j < kb) v -= s[i][j] * x[j];
+      x[i] = v * dinv[i];
+    }
   }
+#pragma unroll
+  for (int i = 0; i < PB; i++)
+    if (i < kb) B[(int64_t)(k + i) * nrhs + c] = x[i];
 }
 
 __global__ void transpose_kernel(const double* __restrict__ A, double* __restrict__ B, int rows, int cols) {
