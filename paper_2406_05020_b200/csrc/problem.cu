@@ -369,7 +369,21 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
   if (!pl.cap) {
     GPFVM_CUDA(cudaStreamCreateWithFlags(&pl.cap, cudaStreamNonBlocking));
     pl.branch.resize(nb);
-    for (int I = 0; I < nb; I++) GPFVM_CUDA(cudaStreamCreateWithFlags(&pl.branch[I], cudaStreamNonBlocking));
+    // The heaviest output block (the PDE-PDE mode products) gets the highest
+    // stream priority: its GEMM waves take the SMs first and the light IC/BC
+    // branches fill the gaps instead of competing for every wave.
+    int lo = 0, hi = 0;
+    GPFVM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool no_prio = getenv("GPFVM_NO_PRIO") != nullptr;
+    int heavy = 0;
+    double best = -1.0;
+    for (int I = 0; I < nb; I++) {
+      double f = 0.0;
+      for (int k : pl.by_out[I]) f += pl.pairs[k].ks.flops_per_rhs();
+      if (f > best) { best = f; heavy = I; }
+    }
+    for (int I = 0; I < nb; I++)
+      GPFVM_CUDA(cudaStreamCreateWithPriority(&pl.branch[I], cudaStreamNonBlocking, (!no_prio && I == heavy) ? hi : lo));
     pl.ev.resize(nb + 1);
     for (auto& e : pl.ev) GPFVM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -390,7 +404,7 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
   }
   GPFVM_CUDA(cudaStreamEndCapture(pl.cap, &graph));
   cudaGraphExec_t exec;
-  GPFVM_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  GPFVM_CUDA(cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority));
   cudaGraphDestroy(graph);
   const int64_t nodes = g_launches.load() - l0;
   g_launches.fetch_sub(nodes);
