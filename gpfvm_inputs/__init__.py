@@ -222,9 +222,17 @@ def _face_blocks(T, X, Y, ht, hx, hy, terms_for_face, jitter, deflate=True):
     return out
 
 
+def wave_analytic_sine(c: float, t, x, y) -> np.ndarray:
+    """u(t,x,y) = cos(sqrt(2) pi c t) sin(pi x) sin(pi y): the solution of
+    u_tt = c^2 (u_xx + u_yy) on [0,1]^2 with u(0) = sin(pi x) sin(pi y),
+    u_t(0) = 0, Dirichlet-0 (the i = j = 1 mode of PAPER.md l.703)."""
+    t, x, y = np.broadcast_arrays(*np.ix_(np.asarray(t, float), np.asarray(x, float), np.asarray(y, float)))
+    return np.cos(np.sqrt(2.0) * np.pi * c * t) * np.sin(np.pi * x) * np.sin(np.pi * y)
+
+
 def wave_problem(nt: int, nx: int, ny: int, *, c: float = 1.0, ell=(0.1, 0.05, 0.05), q: int = 3,
                  centers=None, width: float = 0.05, seed: int = 2, jitter: float = 1e-8,
-                 name: str | None = None) -> Problem:
+                 ic: str = "bump", name: str | None = None) -> Problem:
     """BASELINE config 2: u_tt = c^2 (u_xx + u_yy) on [0,1] x [0,1]^2, Matérn-7/2.
     IC cells: u(0,.) = Gaussian bump (seeded centre, width 0.05) and u_t(0,.) = 0;
     Dirichlet-0 BC cells on the four faces.  `centers` (k x 2) gives a k-RHS
@@ -235,8 +243,13 @@ def wave_problem(nt: int, nx: int, ny: int, *, c: float = 1.0, ell=(0.1, 0.05, 0
         centers = rng.uniform(0.3, 0.7, size=(4, 2))
     T, X, Y = cells(nt), cells(nx), cells(ny)
     ht, hx, hy = 1.0 / nt, 1.0 / nx, 1.0 / ny
-    ic_vals = [np.outer(_gauss_cell_integrals(X.lo, X.hi, cx, width),
-                        _gauss_cell_integrals(Y.lo, Y.hi, cy, width)).ravel() for cx, cy in centers]
+    if ic == "sine":  # u(0,x,y) = sin(pi x) sin(pi y): exact cell integrals
+        sx = (np.cos(np.pi * X.lo) - np.cos(np.pi * X.hi)) / np.pi
+        sy = (np.cos(np.pi * Y.lo) - np.cos(np.pi * Y.hi)) / np.pi
+        ic_vals = [np.outer(sx, sy).ravel()]
+    else:
+        ic_vals = [np.outer(_gauss_cell_integrals(X.lo, X.hi, cx, width),
+                            _gauss_cell_integrals(Y.lo, Y.hi, cy, width)).ravel() for cx, cy in centers]
     blocks = [
         Block("IC_u", [point(0.0), X, Y], [Term(1.0, (0, 0, 0))], jitter * (hx * hy) ** 2, True, ic_vals[0]),
         Block("IC_ut", [point(0.0), X, Y], [Term(1.0, (1, 0, 0))], jitter * (hx * hy) ** 2, True,

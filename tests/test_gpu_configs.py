@@ -111,3 +111,25 @@ def test_3d_solve_reorth_window(window):
     assert np.linalg.norm(G @ a - y) <= 1e-9 * np.linalg.norm(y)
     a_ref = np.linalg.solve(G, y)
     assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
+
+
+def test_wave_sine_solve_predict_vs_oracle_and_analytic():
+    """GPU solve (block-Jacobi FD PCG) + predict on the sine-IC wave problem:
+    posterior mean equals the oracle's Cholesky posterior (1e-8 relative) and
+    the analytic solution within the oracle's own discretisation error."""
+    from oracle.posterior import posterior_exact
+    pts = [np.array([0.2, 0.45, 0.7]), np.array([0.3, 0.5]), np.array([0.35, 0.6])]
+    grid = gi.Grid(pts)
+    p = gi.wave_problem(8, 8, 8, ell=(0.5, 0.3, 0.3), q=3, ic="sine")
+    G = dense_gram(p)
+    y = p.rhs()
+    m_ref, v_ref, _ = posterior_exact(p, grid, G, y)
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    alpha, rep = gp.gpfvm_solve(_t(y), rtol=1e-12, max_iter=3000)
+    assert rep["converged"], rep
+    mean, var = gp.gpfvm_predict(grid, alpha, cov_mode=0)
+    mean = mean.cpu().numpy()
+    assert np.abs(mean - m_ref).max() <= 1e-8 * np.abs(m_ref).max()
+    true = gi.wave_analytic_sine(1.0, *pts).ravel()
+    assert np.abs(mean - true).max() < 2e-2

@@ -119,6 +119,28 @@ def test_heat_posterior_converges_to_analytic_solution():
     assert rate > 1.5, errs
 
 
+def test_wave_posterior_converges_to_analytic_solution():
+    """2D wave equation u_tt = u_xx + u_yy (P:l.694) with the sine initial
+    condition of the paper's wave benchmark (i = j = 1 mode, P:l.703),
+    u_t(0) = 0 and Dirichlet-0 faces: the posterior mean converges to
+    cos(sqrt2 pi t) sin(pi x) sin(pi y) under grid refinement.  Pins the 3D
+    Kronecker Gram, the Matérn-7/2 order-2 functionals and the u_t(0) block."""
+    pts = [np.array([0.2, 0.45, 0.7]), np.array([0.3, 0.5]), np.array([0.35, 0.6])]
+    grid = gi.Grid(pts)
+    true = gi.wave_analytic_sine(1.0, *pts).ravel()
+    errs = []
+    for n in [4, 6, 8, 10]:
+        p = gi.wave_problem(n, n, n, ell=(0.5, 0.3, 0.3), q=3, ic="sine")
+        G = dense_gram(p)
+        m, v, _ = posterior_exact(p, grid, G, p.rhs())
+        errs.append(np.abs(m - true).max())
+        assert v.min() >= -1e-8
+    assert errs[0] > errs[1] > errs[2] > errs[3], errs
+    assert errs[3] < 1e-2, errs
+    rate = np.log(errs[1] / errs[3]) / np.log(10 / 6)
+    assert rate > 3.0, (rate, errs)
+
+
 def test_ic_observations_reproduced():
     """The posterior mean integrated over the IC cells reproduces the IC data
     (noise 1e-8 h^2), i.e. the solve honours the information operator."""
