@@ -559,7 +559,10 @@ int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, in
       GPFVM_CHECK(p->assembled && p->plan, GPFVM_ERR_STATE, "gpfvm_gram_matvec: call gpfvm_assemble_factors first");
       if (!p->pipe[0])
         for (int i = 0; i < 3; i++) GPFVM_CUDA(cudaStreamCreateWithFlags(&p->pipe[i], cudaStreamNonBlocking));
-      const int nch = 4, csz = (nrhs + nch - 1) / nch;
+      // enough chunks that the pipeline tail (last compute + last D2H) is short;
+      // each chunk keeps >= 8 vectors so the DMMA GEMMs stay efficient
+      static const int nch_env = getenv("GPFVM_PIPE_CHUNKS") ? atoi(getenv("GPFVM_PIPE_CHUNKS")) : 0;
+      const int nch = nch_env > 0 ? nch_env : std::max(1, std::min(8, nrhs / 8)), csz = (nrhs + nch - 1) / nch;
       p->stage_in.ensure(n);
       p->stage_out.ensure(n);
       std::vector<cudaEvent_t> evs(2 * nch + 1);
