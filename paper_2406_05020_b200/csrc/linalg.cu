@@ -211,11 +211,11 @@ __device__ __forceinline__ void load_cols(double* __restrict__ Xs, const double*
   const int t = threadIdx.x;
   if ((n & 1) == 0) {
     const int h = n >> 1, total = cnt * h;
-    for (int base = t; base < total; base += 4 * JT) {
+    for (int base = t; base < total; base += 4 * (int)blockDim.x) {
       double2 v[4];
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        int i = base + u * JT;
+        int i = base + u * (int)blockDim.x;
         if (i < total) {
           int c = i / h, r2 = i - c * h;
           v[u] = __ldg(reinterpret_cast<const double2*>(G + (size_t)col_of[c] * n) + r2);
@@ -223,7 +223,7 @@ __device__ __forceinline__ void load_cols(double* __restrict__ Xs, const double*
       }
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        int i = base + u * JT;
+        int i = base + u * (int)blockDim.x;
         if (i < total) {
           int c = i / h, r2 = i - c * h;
           reinterpret_cast<double2*>(Xs + (size_t)c * n)[r2] = v[u];
@@ -231,7 +231,7 @@ __device__ __forceinline__ void load_cols(double* __restrict__ Xs, const double*
       }
     }
   } else {
-    for (int i = t; i < cnt * n; i += JT) {
+    for (int i = t; i < cnt * n; i += blockDim.x) {
       int c = i / n, r = i % n;
       Xs[(size_t)c * n + r] = G[(size_t)col_of[c] * n + r];
     }
@@ -240,14 +240,16 @@ __device__ __forceinline__ void load_cols(double* __restrict__ Xs, const double*
 
 // Xc, Vc: column-major n x n (column j at Xc + j*n).  pairs: (blk_a, blk_b) per CTA.
 template <int JB>
-__global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc, int n, int nblk,
+__global__ void __launch_bounds__(JB <= 8 ? 512 : 256) jacobi_round_kernel(double* Xc, double* Vc, int n, int nblk,
                                                           const int* __restrict__ pairs,
                                                           unsigned long long* offmax,
-                                                          const double* __restrict__ floor_ptr, double skip_tol) {
+                                                          const double* __restrict__ floor_ptr, double skip_tol,
+                                                          int dual) {
   constexpr int JC = 2 * JB;      // columns per CTA (pair of blocks)
   extern __shared__ double sm[];
   double* Xs = sm;                  // [JC][n] column-major (column c at Xs + c*n)
-  double* H = Xs + (size_t)JC * n;  // [JC][JC+1]
+  double* Vs = dual ? Xs + (size_t)JC * n : Xs;  // V columns (dual: own buffer, loaded up front)
+  double* H = Vs + (size_t)JC * n;  // [JC][JC+1]
   double* Q = H + JC * (JC + 1);    // [JC][JC+1]
   __shared__ double cs[JC / 2], sn[JC / 2];
   __shared__ int col_of[JC];
@@ -272,12 +274,13 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
   const int cnt = cnt_s;
   if (cnt < 2) return;
   load_cols(Xs, Xc, n, cnt, col_of);
+  if (dual) load_cols(Vs, Vc, n, cnt, col_of);
   __syncthreads();
   // Gram H = Xs^T Xs: one warp per (a, b) entry, lanes stride the rows
   // (consecutive lanes -> consecutive banks), 4 independent partial sums,
   // shuffle reduction.
   {
-    const int warp = t >> 5, lane = t & 31, nw = JT / 32;
+    const int warp = t >> 5, lane = t & 31, nw = blockDim.x / 32;
     const int npair = cnt * (cnt + 1) / 2;
     for (int e = warp; e < npair; e += nw) {
       const int a = ent_a[e], b = ent_b[e];
@@ -300,9 +303,9 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
       }
     }
   }
-  for (int i = t; i < JC * (JC + 1); i += JT) Q[i] = 0.0;
+  for (int i = t; i < JC * (JC + 1); i += blockDim.x) Q[i] = 0.0;
   __syncthreads();
-  for (int i = t; i < cnt; i += JT) Q[i * (JC + 1) + i] = 1.0;
+  for (int i = t; i < cnt; i += blockDim.x) Q[i * (JC + 1) + i] = 1.0;
   // Convergence measure over all column pairs held by this CTA:
   // |h_ab| / max(sqrt(h_aa h_bb), floor).  floor = tau ||X||_F^2 (0: the
   // classical relative measure) treats pairs of columns that are both below
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
       }
       __syncthreads();
       // columns: H <- H J ; Q <- Q J   (for each pair, each row)
-      for (int i = t; i < (m / 2) * cnt; i += JT) {
+      for (int i = t; i < (m / 2) * cnt; i += blockDim.x) {
         int pr = i / cnt, r = i - pr * cnt;
         int p = pair_ab[pr][0], q = pair_ab[pr][1];
         if (q >= cnt) continue;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
       }
       __syncthreads();
       // rows: H <- J^T H
-      for (int i = t; i < (m / 2) * cnt; i += JT) {
+      for (int i = t; i < (m / 2) * cnt; i += blockDim.x) {
         int pr = i / cnt, r = i - pr * cnt;
         int p = pair_ab[pr][0], q = pair_ab[pr][1];
         if (q >= cnt) continue;
@@ -393,27 +396,33 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(double* Xc, double* Vc
     }
     if (done) break;
   }
-  // X <- X Q, then V <- V Q (V staged through the same shared buffer).  Rows
-  // in parallel; per row JC independent register accumulators (fully unrolled,
-  // no local-memory arrays), operands from shared memory (X column-major:
-  // consecutive rows -> consecutive banks; Q broadcast).  Unused columns
-  // (cnt < JC) carry zeros in Q.
+  // X <- X Q and V <- V Q.  dual: both column sets are resident, all threads
+  // work (thread w < n: row w of X, n <= w < 2n: row w - n of V); otherwise V
+  // is staged through the X buffer in a second pass.  Per row JC independent
+  // register accumulators (fully unrolled), operands from shared memory (column
+  // major: consecutive rows -> consecutive banks; Q broadcast).  Unused
+  // columns (cnt < JC) carry zeros in Q.
+  const int passes = dual ? 1 : 2;
 #pragma unroll 1
-  for (int pass = 0; pass < 2; pass++) {
-    double* dst = pass == 0 ? Xc : Vc;
+  for (int pass = 0; pass < passes; pass++) {
     if (pass == 1) {
       __syncthreads();
       load_cols(Xs, Vc, n, cnt, col_of);
       __syncthreads();
     }
+    const int rows = dual ? 2 * n : n;
 #pragma unroll 1
-    for (int r = t; r < n; r += JT) {
+    for (int w = t; w < rows; w += blockDim.x) {
+      const bool isV = dual ? (w >= n) : (pass == 1);
+      const int r = (dual && w >= n) ? w - n : w;
+      const double* src = (dual && isV) ? Vs : Xs;
+      double* dst = isV ? Vc : Xc;
       double acc[JC];
 #pragma unroll
       for (int j = 0; j < JC; j++) acc[j] = 0.0;
 #pragma unroll 2
       for (int c = 0; c < JC; c++) {
-        const double xv = (c < cnt) ? Xs[(size_t)c * n + r] : 0.0;
+        const double xv = (c < cnt) ? src[(size_t)c * n + r] : 0.0;
 #pragma unroll
         for (int j = 0; j < JC; j++) acc[j] = fma(xv, Q[c * (JC + 1) + j], acc[j]);
       }
@@ -545,6 +554,10 @@ static int jacobi_sweeps(double* Xc, double* Vc, int n, cudaStream_t s) {
   unsigned long long* d_off = reinterpret_cast<unsigned long long*>(off_buf.ptr);
   GPFVM_CUDA(cudaMemcpyAsync(d_pairs, rounds.data(), sizeof(int) * rounds.size(), cudaMemcpyHostToDevice, s));
   size_t smem = sizeof(double) * ((size_t)JC * n + 2 * JC * (JC + 1));
+  const size_t smem_dual = smem + sizeof(double) * (size_t)JC * n;
+  static const bool no_dual = getenv("GPFVM_NO_DUAL") != nullptr;
+  const int dual = (!no_dual && smem_dual <= 200 * 1024) ? 1 : 0;
+  if (dual) smem = smem_dual;
   GPFVM_CHECK(smem <= 220 * 1024, GPFVM_ERR_UNSUPPORTED, "eigensolver: dimension too large");
   {
     // The attribute is per function and device, and sygv runs on several host
@@ -576,6 +589,9 @@ static int jacobi_sweeps(double* Xc, double* Vc, int n, cudaStream_t s) {
     d_floor = fro.ptr;
   }
   const double conv_tol = std::max(4e-15, 2e-16 * n);
+  // 512 threads for the 8-column blocks (measured 36 vs 38 ms on config 1), 256 above (registers)
+  static const int jt_env = getenv("GPFVM_JT") ? atoi(getenv("GPFVM_JT")) : 0;
+  const int jt = jt_env ? std::min(jt_env, JB <= 8 ? 512 : 256) : (JB <= 8 ? 512 : JT);
   int sweeps = 0;
   double offd = 1.0;
   const bool dbg2 = getenv("GPFVM_DEBUG") && atoi(getenv("GPFVM_DEBUG")) > 1;
@@ -583,8 +599,8 @@ static int jacobi_sweeps(double* Xc, double* Vc, int n, cudaStream_t s) {
     sweeps++;
     GPFVM_CUDA(cudaMemsetAsync(d_off, 0, sizeof(unsigned long long), s));
     for (int r = 0; r < players - 1; r++) {
-      jacobi_round_kernel<JB><<<players / 2, JT, smem, s>>>(Xc, Vc, n, nblk, d_pairs + r * players, d_off,
-                                                             d_floor, sweep > 0 ? conv_tol : 0.0);
+      jacobi_round_kernel<JB><<<players / 2, jt, smem, s>>>(Xc, Vc, n, nblk, d_pairs + r * players, d_off,
+                                                             d_floor, sweep > 0 ? conv_tol : 0.0, dual);
       count_launch();
     }
     check_launch("jacobi_round_kernel");
