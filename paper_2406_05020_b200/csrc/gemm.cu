@@ -512,6 +512,22 @@ double gemm_flops(const Gemm& g) {
   return 2.0 * g.M * (double)g.N * g.K * g.nseg * g.batch1 * g.batch2 * g.batch3;
 }
 
+// B (cols x rows) = A^T for A (rows x cols, leading dimension lda), tiled
+__global__ void transpose_any_kernel(const double* __restrict__ A, int64_t lda, double* __restrict__ B, int rows,
+                                     int cols) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = A[(int64_t)r * lda + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) {
+    const int r = bx + j, c = by + threadIdx.x;
+    if (r < cols && c < rows) B[(int64_t)r * rows + c] = tile[threadIdx.x][j];
+  }
+}
+
 void run_gemm(const Gemm& g0, cudaStream_t s) {
   Gemm g = g0;
   // A single-row GEMM batched over right-hand sides that share B is one GEMM
@@ -546,6 +562,23 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
   GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
                     g.N >= 8 && g.K * g.nseg >= 4;
+  if (!fast && g.a_rs == 1 && g.a_cs >= g.M && g.c_cs == 1 && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
+      g.N >= 8 && g.K >= 8 && g.nseg == 1 && g.batch1 * g.batch2 * g.batch3 == 1) {
+    // transposed A (setup GEMMs such as S^T T or L^{-T} L^{-1}): materialise
+    // A^T once (K x M -> M x K) so the tensor-core path applies
+    DevBuf At;
+    At.ensure((size_t)g.M * g.K);
+    const dim3 tg((g.M + 31) / 32, (g.K + 31) / 32);
+    transpose_any_kernel<<<tg, dim3(32, 8), 0, s>>>(g.A, g.a_cs, At.ptr, g.K, g.M);
+    count_launch();
+    Gemm t = g;
+    t.A = At.ptr;
+    t.a_rs = g.K;
+    t.a_cs = 1;
+    run_gemm(t, s);
+    GPFVM_CUDA(cudaStreamSynchronize(s));  // At is returned to the pool on scope exit
+    return;
+  }
   if (!fast) {
     int64_t total = (int64_t)g.M * g.N;
     const int64_t kk = (int64_t)g.K * g.nseg;
