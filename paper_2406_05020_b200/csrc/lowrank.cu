@@ -164,6 +164,47 @@ static void build_modes(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
   check_launch("build_modes");
 }
 
+// Append one coupling (input block J of shape shJ, thin in dim 0 or 1) to the
+// rank-r update of a 2D output block of shape (lr.n0, lr.n1).
+void add_lowrank_part(LowRank& lr, int J, const int* shJ, const std::vector<LowRankTerm>& ts, cudaStream_t s) {
+  LowRank::Part part;
+  part.J = J;
+  part.type = (shJ[0] == 1) ? 0 : 1;
+  part.k0 = lr.rk;
+  part.nin = part.type == 0 ? shJ[1] : shJ[0];
+  part.P = (int)ts.size();
+  const int P = part.P;
+  if (part.type == 0) {
+    part.stk.ensure((size_t)P * lr.n1 * part.nin);
+    part.fixed.ensure((size_t)lr.n0 * P);
+    for (int q = 0; q < P; q++) {  // F0: n0 x 1, F1: n1 x n'_1
+      scaled_copy2<<<gb((int64_t)lr.n1 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n1 * part.nin,
+                                                                 ts[q].F1, 1.0, (int64_t)lr.n1 * part.nin);
+      set_col_kernel<<<gb(lr.n0), 256, 0, s>>>(part.fixed.ptr, P, q, ts[q].F0, lr.n0, ts[q].coef);
+      count_launch(2);
+    }
+  } else {
+    part.stk.ensure((size_t)P * lr.n0 * part.nin);
+    part.fixed.ensure((size_t)P * lr.n1);
+    for (int q = 0; q < P; q++) {  // F0: n0 x n'_0, F1: n1 x 1
+      scaled_copy2<<<gb((int64_t)lr.n0 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n0 * part.nin,
+                                                                 ts[q].F0, ts[q].coef, (int64_t)lr.n0 * part.nin);
+      scaled_copy2<<<gb(lr.n1), 256, 0, s>>>(part.fixed.ptr + (int64_t)q * lr.n1, ts[q].F1, 1.0, lr.n1);
+      count_launch(2);
+    }
+  }
+  lr.rk += P;
+  lr.parts.push_back(std::move(part));
+}
+
+void LowRank::ensure(int Rn) {
+  int pmax = 1;
+  for (const auto& part : parts) pmax = std::max(pmax, part.P);
+  U.ensure((size_t)Rn * n0 * std::max(1, rk));
+  V.ensure((size_t)Rn * std::max(1, rk) * n1);
+  T.ensure((size_t)Rn * pmax * n0);
+}
+
 // Mark and build the low-rank parts of every 2D output block (and the mode
 // updates of d >= 3 output blocks).
 void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
@@ -182,43 +223,15 @@ void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
       PairOp& op = pl.pairs[k];
       const BlockInt& BJ = p->blocks[op.J];
       if (op.J == I || !(BJ.shape[0] == 1 || BJ.shape[1] == 1)) continue;
-      LowRank::Part part;
-      part.J = op.J;
-      part.type = (BJ.shape[0] == 1) ? 0 : 1;
-      part.k0 = lr.rk;
-      part.nin = part.type == 0 ? BJ.shape[1] : BJ.shape[0];
       std::vector<const KronTerm*> ts;
       for (const auto& t : p->terms)
         if (t.I == I && t.J == op.J) ts.push_back(&t);
-      part.P = (int)ts.size();
-      if (part.P == 0) continue;
-      const int P = part.P;
-      if (part.type == 0) {
-        part.stk.ensure((size_t)P * lr.n1 * part.nin);
-        part.fixed.ensure((size_t)lr.n0 * P);
-        for (int q = 0; q < P; q++) {
-          const Factor& F0 = p->factors[ts[q]->fid[0]];  // n0 x 1
-          const Factor& F1 = p->factors[ts[q]->fid[1]];  // n1 x n'_1
-          scaled_copy2<<<gb((int64_t)lr.n1 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n1 * part.nin,
-                                                                     F1.data.ptr, 1.0, (int64_t)lr.n1 * part.nin);
-          set_col_kernel<<<gb(lr.n0), 256, 0, s>>>(part.fixed.ptr, P, q, F0.data.ptr, lr.n0, ts[q]->coef);
-          count_launch(2);
-        }
-      } else {
-        part.stk.ensure((size_t)P * lr.n0 * part.nin);
-        part.fixed.ensure((size_t)P * lr.n1);
-        for (int q = 0; q < P; q++) {
-          const Factor& F0 = p->factors[ts[q]->fid[0]];  // n0 x n'_0
-          const Factor& F1 = p->factors[ts[q]->fid[1]];  // n1 x 1
-          scaled_copy2<<<gb((int64_t)lr.n0 * part.nin), 256, 0, s>>>(part.stk.ptr + (int64_t)q * lr.n0 * part.nin,
-                                                                     F0.data.ptr, ts[q]->coef, (int64_t)lr.n0 * part.nin);
-          scaled_copy2<<<gb(lr.n1), 256, 0, s>>>(part.fixed.ptr + (int64_t)q * lr.n1, F1.data.ptr, 1.0, lr.n1);
-          count_launch(2);
-        }
-      }
-      lr.rk += P;
+      if (ts.empty()) continue;
+      std::vector<LowRankTerm> lt;
+      for (const KronTerm* t : ts)
+        lt.push_back({t->coef, p->factors[t->fid[0]].data.ptr, p->factors[t->fid[1]].data.ptr});
+      add_lowrank_part(lr, op.J, BJ.shape, lt, s);
       op.lowrank = true;
-      lr.parts.push_back(std::move(part));
     }
   }
   check_launch("build_lowrank");

@@ -239,11 +239,29 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
     DevBuf Z;
     Z.ensure((size_t)nb * ng);
     bool first = true;
-    for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
-      const int J = pc.bblocks[jb];
-      if (cp.terms[J].empty()) continue;
-      cross_apply(p, cp, J, 1.0, pc.Linv.ptr + pc.boff[jb], nb, Z.ptr, ng, nb, first ? 0.0 : 1.0, s);
-      first = false;
+    // K_{*b} L^{-T}: every thin deflated block couples to the 2D grid as a
+    // rank-P update, so all of them go into one rank-r GEMM that writes Z once
+    // (instead of one K = 1 expansion pass over Z per block)
+    {
+      LowRank lr;
+      lr.n0 = g0;
+      lr.n1 = g1;
+      std::vector<int64_t> boff(p->blocks.size(), 0);
+      for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
+        const int J = pc.bblocks[jb];
+        boff[J] = pc.boff[jb];
+        if (cp.terms[J].empty()) continue;
+        std::vector<LowRankTerm> lt;
+        for (const auto& t : cp.terms[J])
+          lt.push_back({t.coef, cp.factors[t.fid[0]].data.ptr, cp.factors[t.fid[1]].data.ptr});
+        add_lowrank_part(lr, J, p->blocks[J].shape, lt, s);
+      }
+      if (lr.rk > 0) {
+        lr.ensure(nb);
+        lr.apply(pc.Linv.ptr, nb, Z.ptr, ng, nb, 0.0, boff.data(), s);
+        first = false;
+      }
+      GPFVM_CUDA(cudaStreamSynchronize(s));
     }
     std::vector<double> coefs;
     std::vector<std::vector<const double*>> fs;

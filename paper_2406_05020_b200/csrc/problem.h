@@ -126,7 +126,14 @@ struct LowRank {
   int R = 0;
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, const int64_t* block_off,
              cudaStream_t s);
+  void ensure(int Rn);  // U, V, T for Rn right-hand sides
 };
+struct LowRankTerm {
+  double coef;
+  const double* F0;  // n0 x n'_0 (row-major)
+  const double* F1;  // n1 x n'_1
+};
+void add_lowrank_part(LowRank& lr, int J, const int* shJ, const std::vector<LowRankTerm>& ts, cudaStream_t s);
 
 // d >= 3 output block: couplings from blocks that are singleton in exactly one
 // dimension s (IC planes, boundary faces) are mode-s updates
