@@ -348,7 +348,13 @@ void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, do
   GPFVM_CHECK(d == 2, GPFVM_ERR_UNSUPPORTED, "GPFVM_COV_PRECOND: 2D problems only");
   const int64_t per_row = g.n[1];
   const int64_t nbv = p->pc ? std::max<int64_t>(1, p->pc->nb) : 1;
-  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(12e9 / 8 / (4 * nbv * per_row))));
+  // slab budget from free device memory (up to 48 GB): the first mode product
+  // of the Schur part does not depend on the grid rows, so every extra slab
+  // repeats it — one slab covers config 1's 512 x 1024 grid on a B200
+  size_t free_b = 0, total_b = 0;
+  GPFVM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = std::max(2e9, std::min(48e9, 0.45 * (double)free_b));
+  int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(budget / 8 / (4 * nbv * per_row))));
   for (int r0 = 0; r0 < g.n[0]; r0 += rows) {
     int rr = std::min(rows, g.n[0] - r0);
     CrossPlan cp;
