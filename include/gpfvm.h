@@ -201,6 +201,10 @@ typedef struct {
   int precond;        /* GPFVM_PRECOND_* (default BLOCK_FD) */
   int reorth_window;  /* 0: full reorthogonalisation against every kept direction (default);
                          w > 0: only the last w (w = 1 is the PCG recurrence) */
+  int keep_actions;   /* 1 (default): keep every action d_i, G d_i, eta_i for the IterGP
+                         covariance; 0: keep only a ring of max(1, reorth_window) of them
+                         (device memory O(w N) for long budgeted solves; the ITERGP
+                         variance of gpfvm_predict then covers those actions only) */
 } gpfvm_solve_opts;
 
 typedef struct {

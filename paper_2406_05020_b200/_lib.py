@@ -43,7 +43,8 @@ class ProblemDesc(C.Structure):
 
 
 class SolveOpts(C.Structure):
-    _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int), ("precond", C.c_int), ("reorth_window", C.c_int)]
+    _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int), ("precond", C.c_int), ("reorth_window", C.c_int),
+                ("keep_actions", C.c_int)]
 
 
 class SolveReport(C.Structure):

@@ -129,10 +129,10 @@ class GpfvmProblem:
 
     # ---- §8 row 3
     def gpfvm_solve(self, y, rtol: float = 1e-8, max_iter: int = 1000, precond: int = L.PRECOND_BLOCK_FD,
-                    out=None, reorth_window: int = 0) -> Tuple[object, dict]:
+                    out=None, reorth_window: int = 0, keep_actions: bool = True) -> Tuple[object, dict]:
         if out is None:
             out = torch.empty_like(y) if _is_torch(y) else np.empty_like(y)
-        opts = L.SolveOpts(float(rtol), int(max_iter), int(precond), int(reorth_window))
+        opts = L.SolveOpts(float(rtol), int(max_iter), int(precond), int(reorth_window), int(bool(keep_actions)))
         rep = L.SolveReport()
         L.check(self.lib.gpfvm_solve(self.handle, _ptr(y), _ptr(out), C.byref(opts), C.byref(rep), _stream_of(y)))
         return out, {f: getattr(rep, f) for f, _ in L.SolveReport._fields_}

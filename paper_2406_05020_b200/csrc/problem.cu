@@ -621,7 +621,7 @@ int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
     GPFVM_CHECK(p && y && alpha, GPFVM_ERR_INVALID, "null argument");
     GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_solve: call gpfvm_assemble_factors first");
     GPFVM_CUDA(cudaSetDevice(p->device));
-    gpfvm_solve_opts o{1e-8, 1000, GPFVM_PRECOND_BLOCK_FD, 0};
+    gpfvm_solve_opts o{1e-8, 1000, GPFVM_PRECOND_BLOCK_FD, 0, 1};
     if (opts) o = *opts;
     GPFVM_CHECK(o.rtol >= 0 && o.max_iter >= 0 && o.reorth_window >= 0, GPFVM_ERR_INVALID, "bad solve options");
     gpfvm_solve_report rep{};

@@ -741,29 +741,35 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
     rep.converged = 1;
   }
   std::vector<double> coef;
+  // keep_actions = 0: only a ring of W = max(1, reorth_window) actions is kept
+  // (memory O(W N) for long budgeted solves); the IterGP covariance then
+  // covers those W actions only
+  const bool keep = o.keep_actions != 0;
+  const int W = keep ? 0 : std::max(1, o.reorth_window);
+  int64_t total_it = 0;
   while (!rep.converged && it < o.max_iter) {
     if (nr <= o.rtol * ny) {
       rep.converged = 1;
       break;
     }
-    ensure_krylov(p, K.k + 1, s);
-    double* d = K.d.ptr + (int64_t)K.k * N;
-    double* gd = K.gd.ptr + (int64_t)K.k * N;
-    // s = P^{-1} r ; z = G s  on fixed operands (graph-replayed matvec), then
-    // copied into the Krylov slots
+    const int stored = keep ? K.k : (int)std::min<int64_t>(total_it, W);
+    const int slot = keep ? K.k : (int)(total_it % W);
+    ensure_krylov(p, keep ? K.k + 1 : std::min<int64_t>(total_it + 1, W), s);
+    // s = P^{-1} r ; z = G s  on fixed operands (graph-replayed matvec),
+    // G-orthogonalised there, then copied into the Krylov slot
     p->pcg_s.ensure(N);
     p->pcg_z.ensure(N);
-    if (p->pc) precond_apply(p, r.ptr, p->pcg_s.ptr, s);
-    else copy(p->pcg_s.ptr, r.ptr, N, s);
-    matvec_device(p, p->pcg_s.ptr, p->pcg_z.ptr, 1, N, s);
-    copy(d, p->pcg_s.ptr, N, s);
-    copy(gd, p->pcg_z.ptr, N, s);
-    if (K.k > 0) {
+    double* d = p->pcg_s.ptr;
+    double* gd = p->pcg_z.ptr;
+    if (p->pc) precond_apply(p, r.ptr, d, s);
+    else copy(d, r.ptr, N, s);
+    matvec_device(p, d, gd, 1, N, s);
+    if (stored > 0) {
       // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j over the last
       // `w` kept directions (w = k: full reorthogonalisation, §6 l.475; w = 1: the
       // PCG recurrence, equivalent in exact arithmetic)
-      const int w = (o.reorth_window > 0) ? std::min(o.reorth_window, K.k) : K.k;
-      const int j0 = K.k - w;
+      const int w = keep ? ((o.reorth_window > 0) ? std::min(o.reorth_window, stored) : stored) : stored;
+      const int j0 = stored - w;
       dot_many(K.d.ptr + (int64_t)j0 * N, N, gd, N, w, dsc, s);
       coef.resize(w);
       GPFVM_CUDA(cudaMemcpyAsync(coef.data(), dsc, sizeof(double) * w, cudaMemcpyDeviceToHost, s));
@@ -786,11 +792,21 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
     GPFVM_CUDA(cudaMemcpyAsync(dsc, ha, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
     axpy_many(x, d, N, dsc, 1.0, N, 1, s);
     axpy_many(r.ptr, gd, N, dsc + 1, 1.0, N, 1, s);
-    K.eta.push_back(eta);
-    K.k++;
+    copy(K.d.ptr + (int64_t)slot * N, d, N, s);
+    copy(K.gd.ptr + (int64_t)slot * N, gd, N, s);
+    if (keep) {
+      K.eta.push_back(eta);
+      K.k++;
+    } else {
+      if ((int)K.eta.size() < W) K.eta.resize(W, 0.0);
+      K.eta[slot] = eta;
+      K.k = (int)std::min<int64_t>(total_it + 1, W);
+    }
+    total_it++;
     it++;
     nr = norm2(r.ptr, N, dsc, s);
   }
+  if (!keep && (int)K.eta.size() > K.k) K.eta.resize(K.k);
   if (!rep.converged && nr <= o.rtol * ny) rep.converged = 1;
   rep.iterations = it;
   rep.rel_residual = ny > 0 ? nr / ny : 0.0;

@@ -94,8 +94,8 @@ def test_3d_solve_blockjacobi_fd_vs_cholesky(builder):
     assert np.all(v >= v_ref - 1e-8) and np.all(v <= 1.0 + 1e-12)
 
 
-@pytest.mark.parametrize("window", [1, 8])
-def test_3d_solve_reorth_window(window):
+@pytest.mark.parametrize("window,keep", [(1, True), (8, True), (1, False), (4, False)])
+def test_3d_solve_reorth_window(window, keep):
     """gpfvm_solve_opts.reorth_window (R7): windowed
     reorthogonalisation still converges to the Cholesky solution (w = 1 is the
     plain PCG recurrence, identical to full reorthogonalisation in exact
@@ -105,12 +105,19 @@ def test_3d_solve_reorth_window(window):
     y = p.rhs()
     gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
-    alpha, rep = gp.gpfvm_solve(_t(y), rtol=1e-10, max_iter=4000, reorth_window=window)
+    alpha, rep = gp.gpfvm_solve(_t(y), rtol=1e-10, max_iter=4000, reorth_window=window, keep_actions=keep)
     assert rep["converged"], rep
     a = alpha.cpu().numpy()
     assert np.linalg.norm(G @ a - y) <= 1e-9 * np.linalg.norm(y)
     a_ref = np.linalg.solve(G, y)
     assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
+    # the ITERGP variance of the kept actions is a valid (conservative) bound
+    from oracle.posterior import posterior_exact
+    grid = gi.Grid([np.linspace(0, 1, 4), np.linspace(0, 1, 3), np.linspace(0, 1, 3)])
+    _, v_ref, _ = posterior_exact(p, grid, G, y)
+    _, var = gp.gpfvm_predict(grid, alpha, cov_mode=0)
+    v = var.cpu().numpy()
+    assert np.all(v >= v_ref - 1e-8) and np.all(v <= 1.0 + 1e-12)
 
 
 def test_wave_sine_solve_predict_vs_oracle_and_analytic():
