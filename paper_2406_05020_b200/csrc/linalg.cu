@@ -255,24 +255,21 @@ __global__ void __launch_bounds__(JB <= 8 ? 512 : 256) jacobi_round_kernel(doubl
   __shared__ int col_of[JC];
   __shared__ int pair_ab[JC / 2][2];
   __shared__ unsigned char ent_a[JC * (JC + 1) / 2], ent_b[JC * (JC + 1) / 2];
-  __shared__ int cnt_s;
   const int t = threadIdx.x;
   const int pa = pairs[2 * blockIdx.x], pb = pairs[2 * blockIdx.x + 1];
-  if (t == 0) {
-    int c = 0;
-    for (int b : {pa, pb}) {
-      if (b < 0) continue;
-      int j0 = b * JB, j1 = min(n, j0 + JB);
-      for (int j = j0; j < j1; j++) col_of[c++] = j;
-    }
-    cnt_s = c;
-    int e = 0;
-    for (int a = 0; a < c; a++)
-      for (int b = a; b < c; b++) { ent_a[e] = (unsigned char)a; ent_b[e] = (unsigned char)b; e++; }
+  // column ids and the upper-triangle (a, b) table, computed in parallel
+  const int na = (pa >= 0) ? min(JB, n - pa * JB) : 0;
+  const int nbb = (pb >= 0) ? min(JB, n - pb * JB) : 0;
+  const int cnt = na + nbb;
+  if (cnt < 2) return;
+  if (t < cnt) col_of[t] = (t < na) ? pa * JB + t : pb * JB + (t - na);
+  for (int e = t; e < cnt * (cnt + 1) / 2; e += blockDim.x) {
+    int a = 0, rem = e;
+    while (rem >= cnt - a) { rem -= cnt - a; a++; }
+    ent_a[e] = (unsigned char)a;
+    ent_b[e] = (unsigned char)(a + rem);
   }
   __syncthreads();
-  const int cnt = cnt_s;
-  if (cnt < 2) return;
   load_cols(Xs, Xc, n, cnt, col_of);
   if (dual) load_cols(Vs, Vc, n, cnt, col_of);
   __syncthreads();
@@ -312,28 +309,28 @@ __global__ void __launch_bounds__(JB <= 8 ? 512 : 256) jacobi_round_kernel(doubl
   // the rounding level of the pencil as converged.  A CTA whose pairs are all
   // below skip_tol leaves its columns untouched.
   const double flo = floor_ptr ? *floor_ptr : 0.0;
-  __shared__ double mcta;
-  if (t < 32) {
-    // squared correlations (one reciprocal per pair, one sqrt per CTA: FP64
-    // division and sqrt are long multi-instruction sequences on this path)
+  __shared__ unsigned long long mcta_bits;
+  if (t == 0) mcta_bits = 0ull;
+  __syncthreads();
+  {
+    // squared correlations over the upper-triangle table, all threads (one
+    // reciprocal per pair; max of non-negative doubles via their bit patterns)
     double m = 0.0;
     const double flo2 = flo * flo;
-    for (int i = t; i < cnt * cnt; i += 32) {
-      int a = i / cnt, b = i - (i / cnt) * cnt;
-      if (b <= a) continue;
+    for (int e = t; e < cnt * (cnt + 1) / 2; e += blockDim.x) {
+      const int a = ent_a[e], b = ent_b[e];
+      if (b == a) continue;
       double d2 = fmax(fabs(H[a * (JC + 1) + a] * H[b * (JC + 1) + b]), flo2);
       double hab = H[a * (JC + 1) + b];
       double v = (d2 > 0.0) ? hab * hab * __drcp_rn(d2) : 0.0;
       m = fmax(m, v);
     }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    m = sqrt(m);
-    if (t == 0) {
-      atomicMax(offmax, (unsigned long long)__double_as_longlong(m));
-      mcta = m;
-    }
+    if ((t & 31) == 0 && m > 0.0) atomicMax(&mcta_bits, (unsigned long long)__double_as_longlong(m));
   }
   __syncthreads();
+  const double mcta = sqrt(__longlong_as_double((long long)mcta_bits));
+  if (t == 0) atomicMax(offmax, (unsigned long long)__double_as_longlong(mcta));
   if (mcta < skip_tol) return;
   // parallel cyclic two-sided Jacobi on H (cnt x cnt), round-robin pairing
   const int m = (cnt + 1) & ~1;  // even player count (a dummy if cnt odd)
