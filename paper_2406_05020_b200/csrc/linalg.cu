@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(JB <= 8 ? 512 : 256) jacobi_round_kernel(doubl
     ent_b[e] = (unsigned char)(a + rem);
   }
   __syncthreads();
+  for (int i = t; i < JC * (JC + 1); i += blockDim.x) H[i] = 0.0;  // unused indices stay 0
   load_cols(Xs, Xc, n, cnt, col_of);
   if (dual) load_cols(Vs, Vc, n, cnt, col_of);
   __syncthreads();
@@ -365,29 +366,38 @@ __global__ void __launch_bounds__(JB <= 8 ? 512 : 256) jacobi_round_kernel(doubl
         pair_ab[t][1] = q;
       }
       __syncthreads();
-      // columns: H <- H J ; Q <- Q J   (for each pair, each row)
-      for (int i = t; i < (m / 2) * cnt; i += blockDim.x) {
-        int pr = i / cnt, r = i - pr * cnt;
-        int p = pair_ab[pr][0], q = pair_ab[pr][1];
-        if (q >= cnt) continue;
-        double c = cs[pr], s = sn[pr];
-        double hp = H[r * (JC + 1) + p], hq = H[r * (JC + 1) + q];
-        H[r * (JC + 1) + p] = c * hp - s * hq;
-        H[r * (JC + 1) + q] = s * hp + c * hq;
-        double qp = Q[r * (JC + 1) + p], qq = Q[r * (JC + 1) + q];
-        Q[r * (JC + 1) + p] = c * qp - s * qq;
-        Q[r * (JC + 1) + q] = s * qp + c * qq;
-      }
-      __syncthreads();
-      // rows: H <- J^T H
-      for (int i = t; i < (m / 2) * cnt; i += blockDim.x) {
-        int pr = i / cnt, r = i - pr * cnt;
-        int p = pair_ab[pr][0], q = pair_ab[pr][1];
-        if (q >= cnt) continue;
-        double c = cs[pr], s = sn[pr];
-        double hp = H[p * (JC + 1) + r], hq = H[q * (JC + 1) + r];
-        H[p * (JC + 1) + r] = c * hp - s * hq;
-        H[q * (JC + 1) + r] = s * hp + c * hq;
+      // H <- J^T H J and Q <- Q J in one phase: thread per 2x2 block
+      // H[{p1,q1},{p2,q2}] of a pair of pairs (disjoint, no races) plus the Q
+      // column pairs.  Entries of unused indices (>= cnt) are zero and pairs
+      // touching them rotate by the identity.
+      {
+        const int np2 = m / 2;
+        const int nblk2 = np2 * np2;
+        for (int i = t; i < nblk2 + np2 * cnt; i += blockDim.x) {
+          if (i < nblk2) {
+            const int i1 = i / np2, i2 = i - i1 * np2;
+            const int p1 = pair_ab[i1][0], q1 = pair_ab[i1][1], p2 = pair_ab[i2][0], q2 = pair_ab[i2][1];
+            const double c1 = cs[i1], s1 = sn[i1], c2 = cs[i2], s2 = sn[i2];
+            const double hpp = H[p1 * (JC + 1) + p2], hpq = H[p1 * (JC + 1) + q2];
+            const double hqp = H[q1 * (JC + 1) + p2], hqq = H[q1 * (JC + 1) + q2];
+            // columns (right J2), then rows (left J1^T)
+            const double ap = c2 * hpp - s2 * hpq, aq = s2 * hpp + c2 * hpq;  // row p1
+            const double bp = c2 * hqp - s2 * hqq, bq = s2 * hqp + c2 * hqq;  // row q1
+            H[p1 * (JC + 1) + p2] = c1 * ap - s1 * bp;
+            H[q1 * (JC + 1) + p2] = s1 * ap + c1 * bp;
+            H[p1 * (JC + 1) + q2] = c1 * aq - s1 * bq;
+            H[q1 * (JC + 1) + q2] = s1 * aq + c1 * bq;
+          } else {
+            const int k = i - nblk2;
+            const int pr = k / cnt, r = k - pr * cnt;
+            const int p = pair_ab[pr][0], q = pair_ab[pr][1];
+            if (q >= cnt) continue;
+            const double c = cs[pr], sv = sn[pr];
+            const double qp = Q[r * (JC + 1) + p], qq = Q[r * (JC + 1) + q];
+            Q[r * (JC + 1) + p] = c * qp - sv * qq;
+            Q[r * (JC + 1) + q] = sv * qp + c * qq;
+          }
+        }
       }
       __syncthreads();
     }
