@@ -188,11 +188,18 @@ int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream);
  * al. 2022 Alg. 1, CG policy, full reorthogonalisation §6 l.475): actions
  * s_i = P^{-1} r_{i-1}, G-conjugate directions d_i and eta_i = d_i^T G d_i
  * are kept on the device for the computational-uncertainty downdate used by
- * gpfvm_predict.  P is the block-LDL / fast-diagonalisation preconditioner
- * built on the first call after assembly and cached.
+ * gpfvm_predict.  P is built on the first call after assembly
+ * and cached: for one 2D two-term PDE block with <= 16384 deflated IC/BC
+ * cells, fast diagonalisation of the PDE block + exact block-LDL elimination
+ * of the IC/BC cells (thin blocks: in closed Kronecker form); otherwise
+ * block-Jacobi fast diagonalisation of every block.
  * Stops when ||r||_2 <= rtol ||y||_2 (recursive residual) or after
  * max_iter iterations; the report holds the final true residual too.
- * nrhs must be 1 (multi-RHS systems: call once per column). */
+ * opts may be NULL (defaults below); y, alpha: N-vectors (device or host).
+ * nrhs must be 1 (multi-RHS systems: call once per column).  Errors:
+ * GPFVM_ERR_STATE before assembly, GPFVM_ERR_NUMERIC if the Schur complement
+ * cannot be factorised even after shifting, GPFVM_ERR_UNSUPPORTED for more
+ * than 16384 deflated cells in the exact path. */
 enum { GPFVM_PRECOND_NONE = 0, GPFVM_PRECOND_JACOBI = 1, GPFVM_PRECOND_BLOCK_FD = 2 };
 
 typedef struct {
