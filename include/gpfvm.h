@@ -198,8 +198,8 @@ int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream);
  * opts may be NULL (defaults below); y, alpha: N-vectors (device or host).
  * nrhs must be 1 (multi-RHS systems: call once per column).  Errors:
  * GPFVM_ERR_STATE before assembly, GPFVM_ERR_NUMERIC if the Schur complement
- * cannot be factorised even after shifting, GPFVM_ERR_UNSUPPORTED for more
- * than 16384 deflated cells in the exact path. */
+ * cannot be factorised even after shifting, GPFVM_ERR_CUDA on device errors
+ * (e.g. out of memory for the Krylov store: see keep_actions). */
 enum { GPFVM_PRECOND_NONE = 0, GPFVM_PRECOND_JACOBI = 1, GPFVM_PRECOND_BLOCK_FD = 2 };
 
 typedef struct {
