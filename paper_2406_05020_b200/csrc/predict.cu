@@ -15,6 +15,7 @@
 //              (three GEMMs per pair), and the IC/BC Schur part is
 //              z^T S^{-1} z with z = k_b - Y^T k_p, processed in grid slabs.
 #include <cmath>
+#include <cstdio>
 
 #include "problem.h"
 
@@ -355,6 +356,9 @@ void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, do
   GPFVM_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double budget = std::max(2e9, std::min(48e9, 0.45 * (double)free_b));
   int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(budget / 8 / (4 * nbv * per_row))));
+  if (getenv("GPFVM_DEBUG"))
+    fprintf(stderr, "[gpfvm] predict PRECOND: free %.1f GB, budget %.1f GB, %d rows per slab\n", free_b / 1e9,
+            budget / 1e9, rows);
   for (int r0 = 0; r0 < g.n[0]; r0 += rows) {
     int rr = std::min(rows, g.n[0] - r0);
     CrossPlan cp;
