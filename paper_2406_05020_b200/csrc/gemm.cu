@@ -562,8 +562,13 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
   GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
                     g.N >= 8 && g.K * g.nseg >= 4;
-  if (!fast && g.a_rs == 1 && g.a_cs >= g.M && g.c_cs == 1 && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
-      g.N >= 8 && g.K >= 8 && g.nseg == 1 && g.batch1 * g.batch2 * g.batch3 == 1) {
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  if (!fast) GPFVM_CUDA(cudaStreamIsCapturing(s, &cap_status));
+  if (!fast && cap_status == cudaStreamCaptureStatusNone && g.a_rs == 1 && g.a_cs >= g.M && g.c_cs == 1 &&
+      (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 && g.N >= 8 && g.K >= 8 && g.nseg == 1 &&
+      g.batch1 * g.batch2 * g.batch3 == 1) {
+    // (not while a CUDA graph is being captured: the scratch copy is returned
+    // to the pool after a stream synchronisation)
     // transposed A (setup GEMMs such as S^T T or L^{-T} L^{-1}): materialise
     // A^T once (K x M -> M x K) so the tensor-core path applies
     DevBuf At;

@@ -51,20 +51,35 @@ __global__ void scaled_copy2(double* dst, const double* __restrict__ src, double
 
 // y[r][a][i][b] = beta y[r][a][i][b] + sum_p U[i][p] W[r][p][a][b]   (P <= 16).
 // blockIdx.y walks the (r, a) slabs (each ns*B contiguous doubles of y), the
-// x-dimension the slab: coalesced y and W, U broadcast, 32-bit index math.
+// x-dimension the slab: coalesced y and W, 32-bit index math.  U (ns x P) is
+// staged in shared memory once per CTA; for B = 1 (s = last dimension) the P
+// values W[r][:][a] of a slab are broadcast from shared memory too.
 __global__ void mode_update_kernel(double* __restrict__ y, int64_t ldy, const double* __restrict__ U,
                                    const double* __restrict__ W, int R, int A, int ns, int B, int P, double beta) {
+  extern __shared__ double us[];  // [ns][P], then [P] slab values (B = 1)
+  for (int k = threadIdx.x; k < ns * P; k += blockDim.x) us[k] = U[k];
+  double* wsl = us + (size_t)ns * P;
+  __syncthreads();
   const int slab = ns * B;
   const int64_t AB = (int64_t)A * B;
   for (int ra = blockIdx.y; ra < R * A; ra += gridDim.y) {
     const int r = ra / A, a = ra - r * A;
     double* yr = y + (int64_t)r * ldy + (int64_t)a * slab;
     const double* Wr = W + (int64_t)r * P * AB + (int64_t)a * B;
+    if (B == 1) {
+      __syncthreads();
+      if (threadIdx.x < P) wsl[threadIdx.x] = Wr[(int64_t)threadIdx.x * AB];
+      __syncthreads();
+    }
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < slab; e += gridDim.x * blockDim.x) {
       const int i = e / B, b = e - i * B;
-      const double* Ui = U + (int64_t)i * P;
+      const double* Ui = us + (size_t)i * P;
       double acc = 0.0;
-      for (int q = 0; q < P; q++) acc = fma(__ldg(Ui + q), __ldg(Wr + (int64_t)q * AB + b), acc);
+      if (B == 1) {
+        for (int q = 0; q < P; q++) acc = fma(Ui[q], wsl[q], acc);
+      } else {
+        for (int q = 0; q < P; q++) acc = fma(Ui[q], __ldg(Wr + (int64_t)q * AB + b), acc);
+      }
       yr[e] = (beta != 0.0) ? fma(beta, yr[e], acc) : acc;
     }
   }
@@ -90,8 +105,17 @@ void ModeUpdate::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int
   const int64_t nslab = (int64_t)R * A;
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((slab + bx - 1) / bx, (148 * 16 + nslab - 1) / nslab));
   const int64_t gy = std::min<int64_t>(nslab, std::max<int64_t>(1, 148 * 16 / gx));
-  mode_update_kernel<<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(gy, 65535)), bx, 0, st>>>(y, ldy, U.ptr, W.ptr,
-                                                                                                 R, A, ns, B, P, beta);
+  const size_t smem = sizeof(double) * ((size_t)ns * P + P);
+  if (smem > 48 * 1024) {
+    static bool attr = false;  // per process; the pencil sizes here are small
+    if (!attr) {
+      GPFVM_CUDA(cudaFuncSetAttribute(mode_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    GPFVM_CHECK(smem <= 200 * 1024, GPFVM_ERR_UNSUPPORTED, "mode update: ns * P too large");
+  }
+  mode_update_kernel<<<dim3((unsigned)gx, (unsigned)std::min<int64_t>(gy, 65535)), bx, smem, st>>>(
+      y, ldy, U.ptr, W.ptr, R, A, ns, B, P, beta);
   count_launch();
 }
 
