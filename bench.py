@@ -262,9 +262,9 @@ def main():
     roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
-                "traffic": 0.867e9,
+                "traffic": 0.866e9,
                 "traffic_note": "dram read+write of the two CUTLASS mode-product GEMMs of one 128-RHS matvec, "
-                                "ncu --set full (profiles/r01b_matvec_cutlass_full.txt): 349 MB + 518 MB vs "
+                                "ncu --set full (profiles/r01f_matvec_cutlass_full.txt): 348 MB + 518 MB vs "
                                 "270 MB algorithmic (X in, Y out) - the extra is the 268 MB intermediate Z "
                                 "written by stage 0 and read by stage 1",
                 "flops_per_launch": flops_mv}
