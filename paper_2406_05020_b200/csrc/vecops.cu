@@ -3,6 +3,7 @@
 // same inputs always give bitwise-identical scalars), multi-axpy for the
 // IterGP reorthogonalisation, and element-wise helpers.  All memory-bound,
 // vectorised over a grid sized to 2 x 148 SMs.
+#include <algorithm>
 #include "internal.h"
 
 namespace gpfvm {
@@ -84,10 +85,14 @@ unsigned grid_for(int64_t n, int threads) {
 
 void dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, double* out, cudaStream_t s) {
   if (k <= 0) return;
+  // blocks per dot from the length (>= 4 elements per thread), so short dots
+  // (e.g. the n_b-long rows of S^{-1}) do not launch 296 near-empty CTAs each;
+  // fixed for a given n, hence still deterministic
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (n + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
   static thread_local DevBuf partial;
   partial.ensure((size_t)RED_BLOCKS * k);
-  dot_partial_kernel<<<dim3(RED_BLOCKS, k), RED_THREADS, 0, s>>>(X, ldx, v, n, partial.ptr);
-  dot_final_kernel<<<k, 512, 0, s>>>(partial.ptr, RED_BLOCKS, out);
+  dot_partial_kernel<<<dim3(nblk, k), RED_THREADS, 0, s>>>(X, ldx, v, n, partial.ptr);
+  dot_final_kernel<<<k, 512, 0, s>>>(partial.ptr, nblk, out);
   count_launch(2);
   check_launch("dot_many");
 }
