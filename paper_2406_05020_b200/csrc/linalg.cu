@@ -658,14 +658,14 @@ static void sygv_core(const double* A, const double* Bm, int n, double* V, doubl
   W.ensure((size_t)n * n);
   Wt.ensure((size_t)n * n);
   U.ensure((size_t)n * n);
-  int* d_info;
-  GPFVM_CUDA(cudaMalloc(&d_info, sizeof(int)));
+  DevBuf info_buf;  // pooled: cudaFree would synchronise the whole device
+  info_buf.ensure(1);
+  int* d_info = reinterpret_cast<int*>(info_buf.ptr);
   GPFVM_CUDA(cudaMemcpyAsync(L.ptr, Bm, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
   int info = cholesky_inplace(L.ptr, n, s, d_info);
   GPFVM_CHECK(info == 0, GPFVM_ERR_NUMERIC, "sygv: B factor not positive definite (column " + std::to_string(info) + ")");
   GPFVM_CUDA(cudaMemcpyAsync(W.ptr, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
   int infoA = cholesky_inplace(W.ptr, n, s, d_info);
-  cudaFree(d_info);
   if (infoA == 0) {
     trsm_lower(L.ptr, n, W.ptr, n, s);        // G = L^{-1} M (row-major) == column-major G^T
     jacobi_cols(W.ptr, n, U.ptr, w, true, s);

@@ -550,19 +550,15 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   Lf.ensure((size_t)nb * nb);
   copy(S0.ptr, S.ptr, (int64_t)nb * nb, s);
   std::vector<double> diag(nb);
-  {
-    DevBuf dg;
-    dg.ensure(nb);
-    // fetch max diagonal (host) for the shift scale
-    std::vector<double> hS((size_t)nb * nb);
-    GPFVM_CUDA(cudaMemcpyAsync(hS.data(), S0.ptr, sizeof(double) * nb * nb, cudaMemcpyDeviceToHost, s));
-    GPFVM_CUDA(cudaStreamSynchronize(s));
-    for (int i = 0; i < nb; i++) diag[i] = hS[(size_t)i * nb + i];
-  }
+  // fetch the diagonal only (strided copy) for the shift scale
+  GPFVM_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double), S0.ptr, sizeof(double) * (nb + 1), sizeof(double), nb,
+                               cudaMemcpyDeviceToHost, s));
+  GPFVM_CUDA(cudaStreamSynchronize(s));
   double dmax = 0.0;
   for (double v : diag) dmax = std::max(dmax, v);
-  int* d_info;
-  GPFVM_CUDA(cudaMalloc(&d_info, sizeof(int)));
+  DevBuf info_buf;  // pooled: cudaFree would synchronise the whole device
+  info_buf.ensure(1);
+  int* d_info = reinterpret_cast<int*>(info_buf.ptr);
   double shift = 0.0;
   for (int attempt = 0; attempt < 30; attempt++) {
     copy(Lf.ptr, S0.ptr, (int64_t)nb * nb, s);
@@ -575,7 +571,6 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
     shift = (shift == 0.0) ? 1e-14 * dmax : shift * 10.0;
     GPFVM_CHECK(attempt < 29, GPFVM_ERR_NUMERIC, "block-LDL: Schur complement not SPD even after shifting");
   }
-  cudaFree(d_info);
   pc.shift = shift;
   // explicit L^{-1} (lower triangular; the PRECOND variance uses ||L^{-1} z||^2)
   // and S^{-1} = L^{-T} L^{-1} (nb x nb) so each application is one multi-dot
