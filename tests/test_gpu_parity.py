@@ -195,7 +195,7 @@ def test_config1_fullsize_solve_properties():
     """Full-size config 1: PCG reaches 1e-8 (true residual recomputed by the
     oracle's Kronecker matvec), posterior mean agrees with the oracle's
     cross-covariance rows at sampled grid points and with the analytic heat
-    solution; variance is within [0, prior] up to 1e-6."""
+    solution; PRECOND variance non-negative and small everywhere."""
     p = gi.config1()
     gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
@@ -223,7 +223,9 @@ def test_config1_fullsize_solve_properties():
     true = gi.heat_analytic(p.meta["amps"], 0.1, grid.points[0], grid.points[1]).ravel()
     assert np.sqrt(np.mean((mean - true) ** 2)) < 2e-4
     v = var.cpu().numpy()
-    assert v.min() >= -1e-6 and v.max() <= 1.0 + 1e-12
+    # ||L^{-1} z||^2 form: no cancellation below zero; the domain is observed
+    # everywhere (PDE cells + IC/BC), so the posterior variance is tiny
+    assert v.min() >= -1e-12 and v.max() <= 1e-6, (v.min(), v.max())
 
 
 def test_errors_and_call_order():
