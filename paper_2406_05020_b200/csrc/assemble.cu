@@ -105,6 +105,26 @@ __global__ void factor_kernel(MaternDD K, int kindL, const double* __restrict__ 
                               const double* __restrict__ hiL, int nL, int mL, int kindR,
                               const double* __restrict__ loR, const double* __restrict__ hiR, int nR,
                               int mR, double* __restrict__ out, int64_t ld) {
+  // the polynomial of g_o and B(0), C(0) depend only on (K, o): one thread per
+  // CTA computes them (dd divisions) into shared memory, bitwise the same
+  // values every thread computed before
+  const int o_blk = (kindL == GPFVM_SITE_POINT ? mL : mL - 1) + (kindR == GPFVM_SITE_POINT ? mR : mR - 1);
+  __shared__ dd s_poly[4], s_B0, s_C0;
+  if (threadIdx.x == 0) {
+    dd pl[4];
+    g_poly(K, o_blk, pl);
+    for (int k = 0; k < 4; k++) s_poly[k] = pl[k];
+    s_B0 = dd_make(0.0);
+    s_C0 = dd_make(0.0);
+    if (o_blk < 0) {
+      dd t[4];
+      g_poly(K, -1, t);
+      s_B0 = t[0];
+      g_poly(K, -2, t);
+      s_C0 = t[0];
+    }
+  }
+  __syncthreads();
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)nL * nR) return;
   int j = (int)(idx / nR);
@@ -123,15 +143,8 @@ __global__ void factor_kernel(MaternDD K, int kindL, const double* __restrict__ 
   }
   const int o = oL + oR;
   dd poly[4];
-  g_poly(K, o, poly);
-  dd B0 = dd_make(0.0), C0 = dd_make(0.0);
-  if (o < 0) {
-    dd t[4];
-    g_poly(K, -1, t);
-    B0 = t[0];
-    g_poly(K, -2, t);
-    C0 = t[0];
-  }
+  for (int k = 0; k < 4; k++) poly[k] = s_poly[k];
+  const dd B0 = s_B0, C0 = s_C0;
   dd acc = dd_make(0.0);
   for (int a = 0; a < cL; a++)
     for (int b = 0; b < cR; b++) {
