@@ -151,13 +151,15 @@ class ShardedKron:
 
     def matvec(self, x_local):
         P, W, nt, cw = len(self.coefs), self.world, self.nt, self.cw
-        spatial_in = list(self.shape[1:])
-        spatial_out = [self.c1] + list(self.shape[2:])
-        send = self.ops.empty(W, P, nt, cw)
-        for c in range(W):
-            for p in range(P):
-                fac = [self.factors[p][1][c * self.c1:(c + 1) * self.c1]] + list(self.factors[p][2:])
-                self.ops.kron(spatial_in, spatial_out, [self.coefs[p]], [fac], x_local, send[c, p], nrhs=nt)
+        spatial = list(self.shape[1:])
+        # one spatial Kronecker product per term over all destination chunks
+        # (P library calls instead of W * P), then one permutation into the
+        # all-to-all send layout [dest chunk][term][local time][chunk]
+        full = self.ops.empty(P, nt, self.rest)
+        for p in range(P):
+            fac = [self.factors[p][1]] + list(self.factors[p][2:])
+            self.ops.kron(spatial, spatial, [self.coefs[p]], [fac], x_local, full[p], nrhs=nt)
+        send = self.ops.permute(full, [P, nt, W, cw], [2, 0, 1, 3])
         recv = _all_to_all(send, self.group, W)
         yspace = self.ops.empty(self.shape[0], cw)
         self.ops.gemm(self.A_big, recv.reshape(W * P * nt, cw), yspace)
