@@ -124,10 +124,14 @@ def test_matvec_config1_fullsize_vs_oracle_kronecker():
     K = KroneckerGram(p)
     gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
-    X = gi.random_vectors(p.size, 2, 7)
-    Y = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
+    R = 128                                   # bench.py's block of vectors
+    X = gi.random_vectors(p.size, R, 7)
+    Xt = _t(X)
+    Yt = torch.empty_like(Xt)
     ref = K.matvec(X)
-    _close(Y, ref, 1e-12, elem=False)
+    for call in range(3):                     # direct launch, graph capture, graph replay
+        gp.gpfvm_gram_matvec(Xt, out=Yt)
+        _close(Yt.cpu().numpy(), ref, 1e-12, elem=False)
 
 
 def test_host_pointer_pipeline_config1():
