@@ -140,10 +140,11 @@ def test_host_pointer_pipeline_config1():
     p = gi.config1()
     gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
-    X = np.ascontiguousarray(gi.random_vectors(p.size, 16, 3))
-    Yd = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
-    Yh = gp.gpfvm_gram_matvec(X)
-    assert np.abs(Yh - Yd).max() <= 1e-14 * np.abs(Yd).max()
+    for R in (16, 128, 37):                   # 2 chunks, bench.py's 8 chunks, ragged chunks
+        X = np.ascontiguousarray(gi.random_vectors(p.size, R, 3))
+        Yd = gp.gpfvm_gram_matvec(_t(X)).cpu().numpy()
+        Yh = gp.gpfvm_gram_matvec(X)
+        assert np.abs(Yh - Yd).max() <= 1e-14 * np.abs(Yd).max(), R
 
 
 def test_solve_and_predict_config0():
