@@ -314,8 +314,8 @@ def test_sygv_centrosymmetric_matern_pencil(n, q, ell):
 
 def test_degenerate_cases():
     """Edge cases: zero right-hand side (alpha = 0, converged at once), zero
-    input block (y = 0), a one-cell problem (1 x 1 Gram vs the oracle), a
-    single point observation, predict before solve."""
+    input block (y = 0), a one-cell problem with one IC point (2 x 2 Gram vs
+    the oracle), predict before solve."""
     p = gi.config0()
     gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
@@ -336,6 +336,12 @@ def test_degenerate_cases():
     g1.gpfvm_assemble_factors()
     X = gi.random_vectors(one.size, 3, 5)
     _close(g1.gpfvm_gram_matvec(_t(X)).cpu().numpy(), X @ G.T, 1e-12)
+    grid = gi.Grid([np.array([0.1, 0.2]), np.array([0.15])])
+    # before any solve: ITERGP variance is the prior, PRECOND is a call-order error
+    _, v0 = g1.gpfvm_predict(grid, _t(np.zeros(one.size)), cov_mode=0)
+    assert np.allclose(v0.cpu().numpy(), 1.0)
+    with pytest.raises(GpfvmError, match="solve"):
+        g1.gpfvm_predict(grid, _t(np.zeros(one.size)), cov_mode=1)
     a1, r1 = g1.gpfvm_solve(_t(one.rhs()), rtol=1e-12)
     assert r1["converged"]
     assert np.allclose(a1.cpu().numpy(), np.linalg.solve(G, one.rhs()), rtol=1e-8, atol=0)
