@@ -270,7 +270,7 @@ def main():
                 "flops_per_launch": flops_mv}
 
     sharded = None
-    if world > 1 and not args.no_sharded:
+    if not args.no_sharded:
         # time-sharded PDE-block operator of BASELINE config 3 (8.4M obs): NCCL all-to-all
         # re-partition + one K-concatenated time GEMM per matvec
         try:
@@ -286,7 +286,8 @@ def main():
             for _ in range(2):
                 A.matvec(xs)
             torch.cuda.synchronize()
-            dist.barrier()
+            if world > 1:
+                dist.barrier()
             e0, e1 = ev(), ev()
             e0.record()
             for _ in range(5):
@@ -294,9 +295,11 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             tt = torch.tensor([e0.elapsed_time(e1) / 5], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             npde = shape[0] * shape[1] * shape[2]
-            sharded = {"workload": "config3 PDE block (time-sharded)", "n_obs": int(npde), "ms": float(tt.item()),
+            sharded = {"workload": "config3 PDE block (time-sharded)", "ranks": world, "n_obs": int(npde),
+                       "ms": float(tt.item()),
                        "GB_s": npde * 16 / (tt.item() * 1e-3) / 1e9, "terms": len(coefs),
                        "comm_bytes_per_matvec": (len(coefs) + 1) * npde * 8}
         except Exception as e:  # never break the headline line
