@@ -14,6 +14,7 @@
 //              the FD part is  sum_{tau,tau'} c c' [(Â_tau o Â_tau') D^{-1} (B̂_tau o B̂_tau')^T]
 //              (three GEMMs per pair), and the IC/BC Schur part is
 //              z^T S^{-1} z with z = k_b - Y^T k_p, processed in grid slabs.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -354,7 +355,8 @@ void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, do
   // repeats it — one slab covers config 1's 512 x 1024 grid on a B200
   size_t free_b = 0, total_b = 0;
   GPFVM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = std::max(2e9, std::min(48e9, 0.45 * (double)free_b));
+  // from the device size (deterministic slab plan), capped by what is free
+  const double budget = std::max(2e9, std::min({48e9, 0.3 * (double)total_b, 0.9 * (double)free_b}));
   int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(budget / 8 / (4 * nbv * per_row))));
   if (getenv("GPFVM_DEBUG"))
     fprintf(stderr, "[gpfvm] predict PRECOND: free %.1f GB, budget %.1f GB, %d rows per slab\n", free_b / 1e9,
