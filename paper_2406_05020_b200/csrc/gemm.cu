@@ -349,6 +349,27 @@ __global__ void __launch_bounds__(256) dgemm_gemvn_kernel(Gemm g) {
       const double* As = A + seg * g.a_sg;
       const double* Bs = B + seg * g.b_sg;
       int k = lane;
+      if (g.b_rs == 1 && ((reinterpret_cast<uintptr_t>(As) | reinterpret_cast<uintptr_t>(Bs)) & 15) == 0 &&
+          (g.b_cs & 1) == 0) {
+        // 16-byte loads over full 256-element chunks (lane: elements 2*lane, 2*lane+1
+        // of each 64-wide slice), then the tail with scalar loads
+        const int nfull = g.K / 256;
+        for (int c = 0; c < nfull; c++) {
+          const int k2 = 256 * c + 2 * lane;
+          double2 av[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) av[u] = __ldg(reinterpret_cast<const double2*>(As + k2 + 64 * u));
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int n = 0; n < NN; n++)
+              if (n < g.N) {
+                const double2 bv = __ldg(reinterpret_cast<const double2*>(Bs + k2 + 64 * u + (int64_t)n * g.b_cs));
+                acc[n] = fma(av[u].x, bv.x, fma(av[u].y, bv.y, acc[n]));
+              }
+        }
+        k = 256 * nfull + lane;
+      }
       for (; k + 96 < g.K; k += 128) {
         double av[4];
 #pragma unroll
