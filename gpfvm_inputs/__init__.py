@@ -301,7 +301,7 @@ def config3() -> Problem:
 
 def shallow_water_problem(nt: int, nx: int, ny: int, *, g: float = 9.81, H: float = 1.0,
                           ell=(0.2, 0.1, 0.1), q: int = 2, width: float = 0.08, noise_frac: float = 0.01,
-                          seed: int = 4, jitter: float = 1e-8, name: str | None = None) -> Problem:
+                          seed: int = 4, jitter: float = 1e-8, center=None, name: str | None = None) -> Problem:
     """BASELINE config 4: linearised constant-depth shallow water (PAPER.md
     Eqs. 24-26 with f = k = 0, constant H):
         eta_t + H (u_x + v_y) = 0,   u_t + g eta_x = 0,   v_t + g eta_y = 0
@@ -315,6 +315,8 @@ def shallow_water_problem(nt: int, nx: int, ny: int, *, g: float = 9.81, H: floa
     T, X, Y = cells(nt), cells(nx), cells(ny)
     ht, hx, hy = 1.0 / nt, 1.0 / nx, 1.0 / ny
     cx, cy = rng.uniform(0.35, 0.65, size=2)
+    if center is not None:  # fixed centre (e.g. (0.5, 0.5) for the mirror-symmetry pin)
+        cx, cy = center
     eta0 = np.outer(_gauss_cell_integrals(X.lo, X.hi, cx, width), _gauss_cell_integrals(Y.lo, Y.hi, cy, width)).ravel()
     sd = noise_frac * float(np.std(eta0))
     eta_obs = eta0 + sd * rng.standard_normal(eta0.shape)

@@ -140,3 +140,27 @@ def test_wave_sine_solve_predict_vs_oracle_and_analytic():
     assert np.abs(mean - m_ref).max() <= 1e-8 * np.abs(m_ref).max()
     true = gi.wave_analytic_sine(1.0, *pts).ravel()
     assert np.abs(mean - true).max() < 2e-2
+
+
+def test_shallow_water_mirror_symmetry_gpu():
+    """GPU solve + predict of the centred shallow-water problem: eta is mirror
+    symmetric in x, u antisymmetric (radiation-BC sign lock on the CUDA path),
+    and the means equal the oracle posterior."""
+    from oracle.posterior import posterior_exact
+    p = gi.shallow_water_problem(3, 4, 4, center=(0.5, 0.5), noise_frac=0.0)
+    G = dense_gram(p)
+    y = p.rhs()
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    alpha, rep = gp.gpfvm_solve(_t(y), rtol=1e-12, max_iter=3000)
+    assert rep["converged"], rep
+    ts, xs, ys = np.array([0.2, 0.6]), np.array([0.1, 0.3, 0.7, 0.9]), np.array([0.2, 0.5, 0.8])
+    for out, sign in ((0, 1.0), (1, -1.0)):
+        grid = gi.Grid([ts, xs, ys], output=out)
+        m, _ = gp.gpfvm_predict(grid, alpha, cov_mode=0, want_var=False)
+        m = m.cpu().numpy()
+        m_ref, _, _ = posterior_exact(p, grid, G, y)
+        scale = np.abs(m_ref).max()
+        assert np.abs(m - m_ref).max() <= 1e-8 * scale
+        m3 = m.reshape(2, 4, 3)
+        assert np.abs(m3 - sign * m3[:, ::-1, :]).max() <= 1e-8 * scale

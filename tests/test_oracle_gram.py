@@ -217,3 +217,53 @@ def test_block_ldl_preconditioner_and_pcg_config0():
     assert np.abs(Ks @ tr.x - m).max() <= 1e-9 * np.abs(m).max()
     vp = variance_precond(p, g, P.apply)
     assert np.abs(vp - v).max() <= 1e-10
+
+
+def _sw_means(p):
+    G = dense_gram(p)
+    y = p.rhs()
+    ts, xs, ys = np.array([0.2, 0.6]), np.array([0.1, 0.3, 0.7, 0.9]), np.array([0.2, 0.5, 0.8])
+    out = []
+    for o in (0, 1, 2):
+        m, _, _ = posterior_exact(p, gi.Grid([ts, xs, ys], output=o), G, y)
+        out.append(m.reshape(2, 4, 3))
+    return out
+
+
+def test_shallow_water_mirror_symmetry_locks_radiation_signs():
+    """Linearised shallow water (P:l.746-761) with a centred, noise-free IC on a
+    symmetric grid: the posterior mean of eta and v is mirror-symmetric in x and
+    u antisymmetric (and eta, u symmetric / v antisymmetric in y).  This locks
+    the per-face signs of the radiation conditions (the paper states only the
+    x = 0 face, reading R5/SPEC): flipping one face's sign breaks the symmetry."""
+    p = gi.shallow_water_problem(3, 4, 4, center=(0.5, 0.5), noise_frac=0.0)
+    eta, u, v = _sw_means(p)
+    scale = max(np.abs(eta).max(), np.abs(u).max(), np.abs(v).max())
+    tol = 1e-10 * scale
+    assert np.abs(eta - eta[:, ::-1, :]).max() <= tol and np.abs(eta - eta[:, :, ::-1]).max() <= tol
+    assert np.abs(u + u[:, ::-1, :]).max() <= tol and np.abs(u - u[:, :, ::-1]).max() <= tol
+    assert np.abs(v - v[:, ::-1, :]).max() <= tol and np.abs(v + v[:, :, ::-1]).max() <= tol
+    # a wrong sign on the x = 1 face must be visible
+    bad = gi.shallow_water_problem(3, 4, 4, center=(0.5, 0.5), noise_frac=0.0)
+    for b in bad.blocks:
+        if b.name == "BCx1":
+            b.terms[1] = Term(-b.terms[1].coeff, b.terms[1].order, b.terms[1].output)
+    eta_b, _, _ = _sw_means(bad)
+    assert np.abs(eta_b - eta_b[:, ::-1, :]).max() > 1e3 * tol
+
+
+def test_fvm_functional_tends_to_collocation():
+    """FVM/collocation consistency: (1/h^2) x the interval-interval factor of
+    cells of width h centred at x, y tends to the point-point kernel k(x - y)
+    as h -> 0, at second order (midpoint rule)."""
+    from oracle.gram import factor_matrix
+    kp = (2, 0.3, 1.0)
+    xs = np.array([0.2, 0.55])
+    ref = factor_matrix(kp, gi.points(xs), 0, gi.points(xs), 0)
+    errs = []
+    for h in (0.1, 0.05, 0.025):
+        cells = gi.Sites(gi.INTERVAL, xs - h / 2, xs + h / 2)
+        F = factor_matrix(kp, cells, 0, cells, 0) / h ** 2
+        errs.append(np.abs(F - ref).max())
+    assert errs[0] > errs[1] > errs[2]
+    assert np.log2(errs[1] / errs[2]) > 1.5, errs
