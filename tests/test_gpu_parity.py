@@ -345,3 +345,26 @@ def test_degenerate_cases():
     a1, r1 = g1.gpfvm_solve(_t(one.rhs()), rtol=1e-12)
     assert r1["converged"]
     assert np.allclose(a1.cpu().numpy(), np.linalg.solve(G, one.rhs()), rtol=1e-8, atol=0)
+
+
+def test_itergp_variance_monotone_in_iterations():
+    """IterGP combined variance (Wenger et al. 2022, P:l.299-302) is
+    non-increasing in the iteration count and bounded below by the exact
+    posterior variance (each action is a PSD downdate)."""
+    from oracle.posterior import posterior_exact
+    p = gi.config0()
+    G = dense_gram(p)
+    y = p.rhs()
+    grid = gi.heat_grid(9, 9)
+    _, v_ref, _ = posterior_exact(p, grid, G, y)
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    prev = None
+    for k in (1, 2, 4, 8, 16, 32):
+        alpha, _ = gp.gpfvm_solve(_t(y), rtol=0.0, max_iter=k, precond=0)
+        _, var = gp.gpfvm_predict(grid, alpha, cov_mode=0)
+        v = var.cpu().numpy()
+        assert np.all(v >= v_ref - 1e-10)
+        if prev is not None:
+            assert np.all(v <= prev + 1e-12)
+        prev = v
