@@ -237,7 +237,14 @@ int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
  *     GPFVM_COV_PRECOND C = P^{-1} (the exact posterior when
  *                       P^{-1} = G^{-1}, e.g. the heat operator)
  * mean/var: n_grid = prod n[i] entries, row-major (dim 0 slowest); either
- * may be NULL to skip it.  alpha: the representer weights (length N). */
+ * may be NULL to skip it.  alpha: the representer weights (length N).  Device
+ * or host pointers as everywhere; grid points are host arrays read during the
+ * call.  PRECOND variance is evaluated in grid slabs along dim 0 sized from
+ * the device memory (one slab for config 1's 512 x 1024 grid on a B200).
+ * Errors: GPFVM_ERR_STATE for GPFVM_COV_PRECOND without a preceding
+ * gpfvm_solve with GPFVM_PRECOND_BLOCK_FD; GPFVM_ERR_UNSUPPORTED for
+ * GPFVM_COV_PRECOND with the block-Jacobi (3D / multi-output) preconditioner
+ * or ndim != 2; GPFVM_ERR_INVALID for a bad grid (output out of range). */
 enum { GPFVM_COV_ITERGP = 0, GPFVM_COV_PRECOND = 1 };
 
 typedef struct {
@@ -250,11 +257,12 @@ int gpfvm_predict(gpfvm_problem* p, const gpfvm_grid* grid, const double* alpha,
                   double* var, int cov_mode, void* stream);
 
 /* ---- instrumentation ------------------------------------------------------
- * Kernel-launch counter (every kernel this library launches increments it)
- * and per-kernel-class timing of the last matvec (CUDA events on `stream`). */
+ * Kernel-launch counter: every kernel this library launches increments it
+ * (a replayed matvec graph counts its kernel nodes). */
 int64_t gpfvm_launch_count(void);
-/* flops of one single-vector Gram matvec as executed (after the algebraic
- * term cancellation of DESIGN.md R6), and of its dominant GEMM class. */
+/* Flops of one single-vector Gram matvec as executed (after the algebraic
+ * term cancellation of DESIGN.md R6; low-rank and mode updates counted as
+ * the GEMMs/streams actually run).  0 before assembly. */
 double gpfvm_matvec_flops(const gpfvm_problem* p);
 
 #ifdef __cplusplus
