@@ -61,7 +61,7 @@ __global__ void vmul2(double* x, const double* __restrict__ d, int64_t n) {
 }
 }  // namespace
 
-void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s) {
+void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s, PencilCache* cache) {
   const BlockInt& B = p->blocks[J];
   const int d = p->ndim;
   bf.J = J;
@@ -83,12 +83,18 @@ void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s) {
       eye2<<<1, 32, 0, s>>>(bf.Q[i].ptr, 1);
       count_launch();
     } else {
-      const Factor& A = p->factors[get_factor(p, out, i, J, lo, J, lo)];
-      const Factor& Bm = p->factors[get_factor(p, out, i, J, hi, J, hi)];
+      const int fa = get_factor(p, out, i, J, lo, J, lo), fb = get_factor(p, out, i, J, hi, J, hi);
+      const Factor& A = p->factors[fa];
+      const Factor& Bm = p->factors[fb];
       GPFVM_CHECK(A.data.ptr && Bm.data.ptr, GPFVM_ERR_STATE, "block FD: diagonal factors not assembled");
+      const Sites& st = B.sites[i];
+      const PencilKey key{out, i, lo, lo == hi ? -1 : hi, st.kind, st.lo, st.hi};
       DevBuf w;
       w.ensure(n);
-      if (lo == hi) {
+      if (cache && cache->count(key)) {
+        // same pencil as an earlier block (e.g. the time factors of the faces)
+        GPFVM_CUDA(cudaMemcpyAsync(bf.Q[i].ptr, cache->at(key), sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+      } else if (lo == hi) {
         I.ensure((size_t)n * n);
         eye2<<<gsz((int64_t)n * n), 256, 0, s>>>(I.ptr, n);
         count_launch();
@@ -96,6 +102,7 @@ void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s) {
       } else {
         sygv(A.data.ptr, Bm.data.ptr, n, bf.Q[i].ptr, w.ptr, s);
       }
+      if (cache && !cache->count(key)) (*cache)[key] = bf.Q[i].ptr;
     }
     transpose(bf.Q[i].ptr, bf.Qt[i].ptr, n, n, s);
   }

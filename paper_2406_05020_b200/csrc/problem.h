@@ -229,7 +229,13 @@ void solve_impl(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
 void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var,
                   int cov_mode, cudaStream_t s);
 void destroy_precond(Precond* pc);
-void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s);
+// eigenbases already computed in this preconditioner build, keyed by the
+// pencil's definition: (output, dim, lower order, higher order or -1 for the
+// identity, site kind) and the site endpoints — blocks that share a site list
+// (e.g. the time cells of the faces and of the PDE block) share the basis
+using PencilKey = std::tuple<int, int, int, int, int, std::vector<double>, std::vector<double>>;
+using PencilCache = std::map<PencilKey, const double*>;
+void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s, PencilCache* cache = nullptr);
 void apply_block_fd(const BlockFD& bf, const double* r, double* z, int64_t n, cudaStream_t s);
 
 }  // namespace gpfvm

@@ -632,7 +632,9 @@ static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
     } else {
       pc->blockjacobi = true;
       pc->bj.resize(p->blocks.size());
-      for (int b = 0; b < (int)p->blocks.size(); b++) build_block_fd(p, b, pc->bj[b], s);
+      PencilCache cache;
+      static const bool no_cache = getenv("GPFVM_NO_PENCIL_CACHE") != nullptr;
+      for (int b = 0; b < (int)p->blocks.size(); b++) build_block_fd(p, b, pc->bj[b], s, no_cache ? nullptr : &cache);
       pt.mark("block-Jacobi FD");
     }
   } catch (...) {
