@@ -5,18 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-def cutlass_include():
-    """Vendored CUTLASS/CuTe header tree (flashinfer's copy in this image), or None."""
-    import glob
-    for pat in ["/opt/prime-rl/.venv/lib/python3*/site-packages/flashinfer/data/cutlass/include",
-                os.path.join(os.path.dirname(os.__file__), "site-packages", "flashinfer", "data", "cutlass", "include")]:
-        for d in glob.glob(pat):
-            if os.path.exists(os.path.join(d, "cutlass", "gemm", "device", "gemm_batched.h")):
-                return d
-    return None
-
-
-SOURCES = ["pool.cu", "assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "cutlass_gemm.cu"]
+SOURCES = ["pool.cu", "assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "gemm_tma.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",
          "-Xcompiler", "-fPIC"]
 
@@ -31,14 +20,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if all(os.path.getmtime(f) <= t for f in srcs + hdrs):
             return out
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    extra = []
-    inc = cutlass_include()
-    if inc:
-        extra = ["-DGPFVM_WITH_CUTLASS", "-I" + inc, "--expt-relaxed-constexpr", "-Xcudafe", "--diag_suppress=20013"]
-    cmd = [nvcc] + FLAGS + extra + ["-o", out] + srcs
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = os.path.join(os.path.dirname(HERE), "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    jobs = []
+    for src in srcs:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc] + cflags + ["-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        jobs.append((obj, subprocess.Popen(cmd)))
+    failed = [obj for obj, p in jobs if p.wait() != 0]
+    if failed:
+        raise RuntimeError("nvcc failed for " + ", ".join(os.path.basename(f) for f in failed))
+    link = [nvcc] + FLAGS + ["-o", out] + [obj for obj, _ in jobs]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+        print(" ".join(link))
+    subprocess.run(link, check=True)
     return out
 
 

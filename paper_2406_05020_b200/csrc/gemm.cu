@@ -550,6 +550,21 @@ __global__ void transpose_any_kernel(const double* __restrict__ A, int64_t lda, 
 }
 
 void run_gemm(const Gemm& g0, cudaStream_t s) {
+  if (g0.K2 > 0) {
+    // extra low-rank term: fused into the TMA kernel's k loop, else a second GEMM
+    if (try_tma_gemm(g0, s)) return;
+    Gemm m = g0;
+    m.K2 = 0;
+    run_gemm(m, s);
+    Gemm e;
+    e.M = g0.M; e.N = g0.N; e.K = g0.K2; e.batch1 = g0.batch1;
+    e.A = g0.A2; e.a_rs = g0.a2_rs; e.a_cs = 1; e.a_b1 = g0.a2_b1;
+    e.B = g0.B2; e.b_rs = 1; e.b_cs = g0.b2_rs; e.b_b1 = g0.b2_b1;
+    e.C = g0.C; e.c_rs = g0.c_rs; e.c_cs = g0.c_cs; e.c_b1 = g0.c_b1;
+    e.alpha = g0.alpha; e.beta = 1.0;
+    run_gemm(e, s);
+    return;
+  }
   Gemm g = g0;
   // A single-row GEMM batched over right-hand sides that share B is one GEMM
   // with the batch as its M dimension (e.g. IC-block contractions).
@@ -662,7 +677,7 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
     check_launch("dgemm_generic_kernel");
     return;
   }
-  if (try_cutlass_gemm(g, s)) return;
+  if (try_tma_gemm(g, s)) return;
   const bool brow = (g.b_cs == 1);
   const int64_t b_ld = brow ? g.b_rs : g.b_cs;
   const bool v16 = aligned16(g.A) && aligned16(g.B) && even(g.a_rs) && even(b_ld) && even(g.a_b1) &&

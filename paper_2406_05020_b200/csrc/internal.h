@@ -106,9 +106,17 @@ struct Gemm {
   double* C = nullptr;
   int64_t c_rs = 0, c_cs = 0, c_b1 = 0, c_b2 = 0, c_b3 = 0;
   double alpha = 1.0, beta = 0.0;
+  // optional extra term  C[b] += alpha * A2[b] B2[b]^T  (A2: M x K2 rows a2_rs,
+  // B2: N x K2 rows b2_rs, both K-contiguous, one batch level): a low-rank
+  // update appended to the contraction as extra k-tiles
+  int K2 = 0;
+  const double* A2 = nullptr;
+  int64_t a2_rs = 0, a2_b1 = 0;
+  const double* B2 = nullptr;
+  int64_t b2_rs = 0, b2_b1 = 0;
 };
 void run_gemm(const Gemm& g, cudaStream_t s);
-bool try_cutlass_gemm(const Gemm& g, cudaStream_t s);  // cutlass_gemm.cu
+bool try_tma_gemm(const Gemm& g, cudaStream_t s);  // gemm_tma.cu (TMA + mbarrier DMMA kernel)
 double gemm_flops(const Gemm& g);
 
 // ---- small dense linear algebra (linalg.cu) ---------------------------------------

@@ -172,7 +172,21 @@ double KronSum::flops_per_rhs() const {
 }
 
 void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-                    cudaStream_t s) const {
+                    cudaStream_t s, const Gemm* extra) const {
+  if (extra && extra->K2 > 0 && !(d == 2 && !rev && P > 0)) {
+    // not fusable here: the Kronecker sum, then the low-rank term as its own GEMM
+    apply(x, ldx, y, ldy, R, beta, w0, w1, s, nullptr);
+    Gemm e;
+    e.M = d == 2 ? nout[0] : 1; e.N = nout[d - 1];
+    for (int k = 1; k < d - 1; k++) e.M *= nout[k];
+    e.K = extra->K2; e.batch1 = R;
+    e.A = extra->A2; e.a_rs = extra->a2_rs; e.a_cs = 1; e.a_b1 = extra->a2_b1;
+    e.B = extra->B2; e.b_rs = 1; e.b_cs = extra->b2_rs; e.b_b1 = extra->b2_b1;
+    e.C = y; e.c_rs = nout[d - 1]; e.c_cs = 1; e.c_b1 = ldy;
+    e.beta = 1.0;
+    run_gemm(e, s);
+    return;
+  }
   if (P == 0) {
     if (beta == 0.0) {
       int64_t osz = 1;
@@ -220,6 +234,11 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     g1.C = y; g1.c_rs = nout[1]; g1.c_cs = 1; g1.c_b1 = ldy;
     g1.batch1 = R;
     g1.beta = beta;
+    if (extra && extra->K2 > 0) {
+      g1.K2 = extra->K2;
+      g1.A2 = extra->A2; g1.a2_rs = extra->a2_rs; g1.a2_b1 = extra->a2_b1;
+      g1.B2 = extra->B2; g1.b2_rs = extra->b2_rs; g1.b2_b1 = extra->b2_b1;
+    }
     run_gemm(g0, s);
     run_gemm(g1, s);
     return;

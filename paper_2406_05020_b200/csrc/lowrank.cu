@@ -11,7 +11,7 @@ unsigned gb(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>
 __global__ void set_col_kernel(double* fixed, int P, int p, const double* __restrict__ src, int n, double c) {
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) fixed[(int64_t)m * P + p] = c * src[m];
 }
-// U[r][m][k0+p] = fixed[m][p]
+// U[r][m][k0+p] = fixed[m][p]   (rk = row stride)
 __global__ void bcast_cols_kernel(double* U, int R, int n0, int rk, int k0, int P, const double* __restrict__ fixed) {
   int64_t total = (int64_t)R * n0 * P;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -32,15 +32,14 @@ __global__ void scatter_cols_kernel(double* U, const double* __restrict__ T, int
     U[(r * n0 + m) * rk + k0 + p] = T[i];
   }
 }
-// V[r][k0+p][n] = fixed[p][n]
-__global__ void bcast_rows_kernel(double* V, int R, int rk, int n1, int k0, int P, const double* __restrict__ fixed) {
-  int64_t total = (int64_t)R * P * n1;
+// Vt[r][n][k0+p] = fixed[p][n]   (V stored transposed, row stride rk)
+__global__ void bcast_vt_kernel(double* Vt, int R, int rk, int n1, int k0, int P, const double* __restrict__ fixed) {
+  int64_t total = (int64_t)R * n1 * P;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    int n = (int)(i % n1);
-    int64_t rp = i / n1;
-    int p = (int)(rp % P);
-    int64_t r = rp / P;
-    V[(r * rk + k0 + p) * n1 + n] = fixed[(int64_t)p * n1 + n];
+    int p = (int)(i % P);
+    int64_t rn = i / P;
+    int n = (int)(rn % n1);
+    Vt[rn * rk + k0 + p] = fixed[(int64_t)p * n1 + n];
   }
 }
 __global__ void scaled_copy2(double* dst, const double* __restrict__ src, double c, int64_t n) {
@@ -224,9 +223,10 @@ void add_lowrank_part(LowRank& lr, int J, const int* shJ, const std::vector<LowR
 void LowRank::ensure(int Rn) {
   int pmax = 1;
   for (const auto& part : parts) pmax = std::max(pmax, part.P);
-  U.ensure((size_t)Rn * n0 * std::max(1, rk));
-  V.ensure((size_t)Rn * std::max(1, rk) * n1);
-  T.ensure((size_t)Rn * pmax * n0);
+  const int kp = std::max(2, rkp());
+  U.ensure((size_t)Rn * n0 * kp);
+  V.ensure((size_t)Rn * n1 * kp);
+  T.ensure((size_t)Rn * pmax * std::max(n0, n1));
 }
 
 // Mark and build the low-rank parts of every 2D output block (and the mode
@@ -261,8 +261,8 @@ void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
   check_launch("build_lowrank");
 }
 
-void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn, double beta, const int64_t* block_off,
-                    cudaStream_t s) {
+void LowRank::prepare(const double* x, int64_t ldx, int Rn, const int64_t* block_off, cudaStream_t s) {
+  const int kp = rkp();
   for (const Part& part : parts) {
     const double* xJ = x + block_off[part.J];
     const int P = part.P;
@@ -270,27 +270,42 @@ void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn
     g.M = Rn; g.K = part.nin;
     g.A = xJ; g.a_rs = ldx; g.a_cs = 1;
     g.B = part.stk.ptr; g.b_rs = 1; g.b_cs = part.nin;
+    g.C = T.ptr; g.c_cs = 1;
     if (part.type == 0) {
-      g.N = P * n1;                                   // V[r][k0+p][:] = F1^p x_J
-      g.C = V.ptr + (int64_t)part.k0 * n1; g.c_rs = (int64_t)rk * n1; g.c_cs = 1;
+      g.N = P * n1;  // T[r][p][:] = F1^p x_J  ->  Vt[r][:][k0+p]
+      g.c_rs = (int64_t)P * n1;
       run_gemm(g, s);
-      bcast_cols_kernel<<<gb((int64_t)Rn * n0 * P), 256, 0, s>>>(U.ptr, Rn, n0, rk, part.k0, P, part.fixed.ptr);
+      scatter_cols_kernel<<<gb((int64_t)Rn * P * n1), 256, 0, s>>>(V.ptr, T.ptr, Rn, n1, kp, part.k0, P);
+      bcast_cols_kernel<<<gb((int64_t)Rn * n0 * P), 256, 0, s>>>(U.ptr, Rn, n0, kp, part.k0, P, part.fixed.ptr);
     } else {
-      g.N = P * n0;                                   // T[r][p][:] = c_p F0^p x_J
-      g.C = T.ptr; g.c_rs = (int64_t)P * n0; g.c_cs = 1;
+      g.N = P * n0;  // T[r][p][:] = c_p F0^p x_J  ->  U[r][:][k0+p]
+      g.c_rs = (int64_t)P * n0;
       run_gemm(g, s);
-      scatter_cols_kernel<<<gb((int64_t)Rn * P * n0), 256, 0, s>>>(U.ptr, T.ptr, Rn, n0, rk, part.k0, P);
-      bcast_rows_kernel<<<gb((int64_t)Rn * P * n1), 256, 0, s>>>(V.ptr, Rn, rk, n1, part.k0, P, part.fixed.ptr);
-      count_launch();
+      scatter_cols_kernel<<<gb((int64_t)Rn * P * n0), 256, 0, s>>>(U.ptr, T.ptr, Rn, n0, kp, part.k0, P);
+      bcast_vt_kernel<<<gb((int64_t)Rn * P * n1), 256, 0, s>>>(V.ptr, Rn, kp, n1, part.k0, P, part.fixed.ptr);
     }
-    count_launch();
+    count_launch(2);
   }
-  // y_r = beta y_r + U_r V_r   (n0 x rk) (rk x n1)  (a streaming kernel was
-  // measured slower than this DMMA GEMM, which keeps V tiles in shared memory)
+  check_launch("LowRank::prepare");
+}
+
+void LowRank::as_extra(Gemm& g, int Rn) const {
+  const int kp = rkp();
+  g.K2 = rk;
+  g.A2 = U.ptr; g.a2_rs = kp; g.a2_b1 = (int64_t)n0 * kp;
+  g.B2 = V.ptr; g.b2_rs = kp; g.b2_b1 = (int64_t)n1 * kp;
+  (void)Rn;
+}
+
+void LowRank::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int Rn, double beta, const int64_t* block_off,
+                    cudaStream_t s) {
+  prepare(x, ldx, Rn, block_off, s);
+  // y_r = beta y_r + U_r V_r^T   (n0 x rk) (rk x n1)
+  const int kp = rkp();
   Gemm g;
   g.M = n0; g.N = n1; g.K = rk;
-  g.A = U.ptr; g.a_rs = rk; g.a_cs = 1; g.a_b1 = (int64_t)n0 * rk;
-  g.B = V.ptr; g.b_rs = n1; g.b_cs = 1; g.b_b1 = (int64_t)rk * n1;
+  g.A = U.ptr; g.a_rs = kp; g.a_cs = 1; g.a_b1 = (int64_t)n0 * kp;
+  g.B = V.ptr; g.b_rs = 1; g.b_cs = kp; g.b_b1 = (int64_t)n1 * kp;
   g.C = y; g.c_rs = n1; g.c_cs = 1; g.c_b1 = ldy;
   g.batch1 = Rn;
   g.beta = beta;

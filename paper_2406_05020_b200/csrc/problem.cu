@@ -285,9 +285,21 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
   bool overwrite = (B.noise == 0.0) && !pl.by_out[I].empty();
   if (!overwrite) vec_scale_add(y + B.offset, x + B.offset, p->noise.ptr + B.offset, B.size, nrhs, ld, s);
   LowRank& lr = pl.lowrank[I];
+  // the rank-rk IC/BC coupling update is fused into the last contraction of
+  // the block's own (diagonal) Kronecker sum when there is one
+  const PairOp* diag = nullptr;
+  for (int k : pl.by_out[I])
+    if (pl.pairs[k].J == I && !pl.pairs[k].lowrank) diag = &pl.pairs[k];
+  static const bool no_fuse = getenv("GPFVM_NO_LRFUSE") != nullptr;
+  Gemm lr_extra;
   if (lr.rk > 0) {
-    lr.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), s);
-    overwrite = false;
+    if (diag && !no_fuse) {
+      lr.prepare(x, ld, nrhs, pl.block_off.data(), s);
+      lr.as_extra(lr_extra, nrhs);
+    } else {
+      lr.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), s);
+      overwrite = false;
+    }
   }
   for (const auto& mu : pl.modes[I]) {
     if (mu.P == 0) continue;
@@ -298,7 +310,7 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
     const PairOp& op = pl.pairs[k];
     if (op.lowrank) continue;
     op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr,
-                pl.w1[I].ptr, s);
+                pl.w1[I].ptr, s, (&op == diag && lr_extra.K2 > 0) ? &lr_extra : nullptr);
     overwrite = false;
   }
 }
@@ -326,7 +338,9 @@ static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
     if (lr.rk > 0) {
       int pmax = 1;
       for (const auto& part : lr.parts) pmax = std::max(pmax, part.P);
-      size_t nu = (size_t)nrhs * lr.n0 * lr.rk, nv = (size_t)nrhs * lr.rk * lr.n1, nt = (size_t)nrhs * pmax * lr.n0;
+      const size_t kp = std::max(2, lr.rkp());
+      size_t nu = (size_t)nrhs * lr.n0 * kp, nv = (size_t)nrhs * lr.n1 * kp,
+             nt = (size_t)nrhs * pmax * std::max(lr.n0, lr.n1);
       if (lr.U.n < nu || lr.V.n < nv || lr.T.n < nt) {
         pl.release_graphs();
         lr.U.ensure(nu);

@@ -48,8 +48,10 @@ struct KronSum {
   int64_t workspace_per_rhs() const;
   double flops_per_rhs() const;
   // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
+  // extra: optional low-rank term (Gemm::K2 fields) added to the result, fused
+  // into the last contraction where its layout allows (2D forward order)
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-             cudaStream_t s) const;
+             cudaStream_t s, const Gemm* extra = nullptr) const;
 };
 
 // Per-block fast-diagonalisation (bjfd.cu)
@@ -122,8 +124,13 @@ struct LowRank {
   };
   int n0 = 0, n1 = 0, rk = 0;
   std::vector<Part> parts;
-  DevBuf U, V, T;
+  DevBuf U, V, T;  // U [R][n0][rkp], V (transposed) [R][n1][rkp], scratch T
   int R = 0;
+  int rkp() const { return (rk + 1) & ~1; }  // even row stride (16-byte TMA strides)
+  // U and V of y += U V^T for the current input (the coupling GEMMs)
+  void prepare(const double* x, int64_t ldx, int Rn, const int64_t* block_off, cudaStream_t s);
+  // the update as the extra term of g (fused into g's k loop)
+  void as_extra(Gemm& g, int Rn) const;
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, const int64_t* block_off,
              cudaStream_t s);
   void ensure(int Rn);  // U, V, T for Rn right-hand sides
