@@ -280,6 +280,8 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
 
 static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
   MatvecPlan& pl = *p->plan;
+  static const int only = getenv("GPFVM_TIMING_ONLY_BRANCH") ? atoi(getenv("GPFVM_TIMING_ONLY_BRANCH")) : -1;
+  if (only >= 0 && I != only) return;  // timing experiments only: wrong results
   const BlockInt& B = p->blocks[I];
   // noise-free block: the first pair overwrites (beta = 0), saving one read-modify-write pass
   bool overwrite = (B.noise == 0.0) && !pl.by_out[I].empty();
