@@ -200,7 +200,7 @@ int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream);
  * GPFVM_ERR_STATE before assembly, GPFVM_ERR_NUMERIC if the Schur complement
  * cannot be factorised even after shifting, GPFVM_ERR_CUDA on device errors
  * (e.g. out of memory for the Krylov store: see keep_actions). */
-enum { GPFVM_PRECOND_NONE = 0, GPFVM_PRECOND_JACOBI = 1, GPFVM_PRECOND_BLOCK_FD = 2 };
+enum { GPFVM_PRECOND_NONE = 0, GPFVM_PRECOND_BLOCK_FD = 2 };  /* 1 is reserved */
 
 typedef struct {
   double rtol;        /* default 1e-8 */

@@ -14,7 +14,7 @@ MAX_TERMS = 16
 
 SITE_POINT = 0
 SITE_INTERVAL = 1
-PRECOND_NONE, PRECOND_JACOBI, PRECOND_BLOCK_FD = 0, 1, 2
+PRECOND_NONE, PRECOND_BLOCK_FD = 0, 2
 COV_ITERGP, COV_PRECOND = 0, 1
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgpfvm.so")

@@ -33,11 +33,19 @@ def _stream_of(x) -> C.c_void_p:
     return C.c_void_p(0)
 
 
-def _ptr(x):
+def _ptr(x, min_numel: int = 0, name: str = "array"):
+    """Raw pointer of an fp64 C-contiguous torch tensor or numpy array holding
+    at least min_numel elements (the library reads/writes through it)."""
     if _is_torch(x):
-        assert x.dtype == torch.float64 and x.is_contiguous(), "fp64 contiguous tensors only"
+        if x.dtype != torch.float64 or not x.is_contiguous():
+            raise ValueError(f"{name}: fp64 contiguous tensors only")
+        if x.numel() < min_numel:
+            raise ValueError(f"{name}: {x.numel()} elements, need {min_numel}")
         return C.c_void_p(x.data_ptr())
-    assert isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags["C_CONTIGUOUS"]
+    if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags["C_CONTIGUOUS"]):
+        raise ValueError(f"{name}: fp64 C-contiguous numpy arrays only")
+    if x.size < min_numel:
+        raise ValueError(f"{name}: {x.size} elements, need {min_numel}")
     return C.c_void_p(x.ctypes.data)
 
 
@@ -124,7 +132,10 @@ class GpfvmProblem:
         nrhs = x.shape[0] if two_d else 1
         if out is None:
             out = torch.empty_like(x) if _is_torch(x) else np.empty_like(x)
-        L.check(self.lib.gpfvm_gram_matvec(self.handle, _ptr(x), _ptr(out), int(nrhs), int(self.N), _stream_of(x)))
+        if (x.shape[-1] if x.ndim else 0) != self.N:
+            raise ValueError(f"x: last dimension {x.shape[-1] if x.ndim else 0}, expected N = {self.N}")
+        L.check(self.lib.gpfvm_gram_matvec(self.handle, _ptr(x, nrhs * self.N, "x"), _ptr(out, nrhs * self.N, "out"),
+                                           int(nrhs), int(self.N), _stream_of(x)))
         return out
 
     # ---- §8 row 3
@@ -134,7 +145,8 @@ class GpfvmProblem:
             out = torch.empty_like(y) if _is_torch(y) else np.empty_like(y)
         opts = L.SolveOpts(float(rtol), int(max_iter), int(precond), int(reorth_window), int(bool(keep_actions)))
         rep = L.SolveReport()
-        L.check(self.lib.gpfvm_solve(self.handle, _ptr(y), _ptr(out), C.byref(opts), C.byref(rep), _stream_of(y)))
+        L.check(self.lib.gpfvm_solve(self.handle, _ptr(y, self.N, "y"), _ptr(out, self.N, "out"), C.byref(opts),
+                                     C.byref(rep), _stream_of(y)))
         return out, {f: getattr(rep, f) for f, _ in L.SolveReport._fields_}
 
     # ---- §8 row 4
@@ -158,9 +170,9 @@ class GpfvmProblem:
                 mean = np.empty(ng)
             if want_var and var is None:
                 var = np.empty(ng)
-        L.check(self.lib.gpfvm_predict(self.handle, C.byref(g), _ptr(alpha),
-                                       _ptr(mean) if want_mean else C.c_void_p(0),
-                                       _ptr(var) if want_var else C.c_void_p(0), int(cov_mode),
+        L.check(self.lib.gpfvm_predict(self.handle, C.byref(g), _ptr(alpha, self.N, "alpha"),
+                                       _ptr(mean, ng, "mean") if want_mean else C.c_void_p(0),
+                                       _ptr(var, ng, "var") if want_var else C.c_void_p(0), int(cov_mode),
                                        _stream_of(alpha)))
         return mean, var
 

@@ -43,35 +43,42 @@ void check_launch(const char* what);
 // block is handed out again only to a later allocation; temporaries are
 // released after the stream that used them has been synchronised or when the
 // next user is on the same stream (stream order), as everywhere in this library.
-void* pool_alloc(size_t bytes);
-void pool_free(void* p, size_t bytes);
+void* pool_alloc(size_t bytes);              // on the current device
+void pool_free(void* p, size_t bytes, int dev);  // back to the bucket of the device it came from
 void pool_trim();  // cudaFree every cached block of the current device
+int current_device();
 
 struct DevBuf {
   double* ptr = nullptr;
   size_t n = 0;
+  int dev = -1;  // device the block was allocated on
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n) { o.ptr = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n), dev(o.dev) { o.ptr = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); ptr = o.ptr; n = o.n; o.ptr = nullptr; o.n = 0; }
+    if (this != &o) { release(); ptr = o.ptr; n = o.n; dev = o.dev; o.ptr = nullptr; o.n = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) pool_free(ptr, n * sizeof(double));
+    if (ptr) pool_free(ptr, n * sizeof(double), dev);
     ptr = nullptr;
     n = 0;
   }
   void ensure(size_t count) {
-    if (count <= n) return;
+    if (count <= n && (ptr == nullptr || dev == current_device())) return;
     release();
     if (count == 0) return;
     ptr = static_cast<double*>(pool_alloc(count * sizeof(double)));
     n = count;
+    dev = current_device();
   }
 };
+// Scratch buffer private to (calling thread, current device, stream, slot):
+// library-internal temporaries of stream-ordered calls (no sharing across
+// devices or concurrently used streams).
+DevBuf& scratch(cudaStream_t s, int slot);
 
 // ---- Matérn parameters in double-double ----------------------------------------
 struct MaternDD {

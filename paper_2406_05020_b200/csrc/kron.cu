@@ -16,6 +16,7 @@
 // K-segment GEMM  Y_r = sum_p X_r (c_p F^p)^T.  Coefficients are folded into
 // the first-applied factor.
 #include <algorithm>
+#include <map>
 #include <cstdlib>
 
 #include "problem.h"
@@ -417,8 +418,10 @@ int guarded_kron(int ndim, const int* in_shape, const int* out_shape, int P, con
       std::vector<const double*> key_f;
       std::unique_ptr<KronSum> ks;
     };
-    static thread_local std::vector<Entry> cache;
-    static thread_local DevBuf w0, w1;
+    static thread_local std::map<int, std::vector<Entry>> caches;  // per device
+    std::vector<Entry>& cache = caches[current_device()];
+    DevBuf& w0 = scratch(s, 1);
+    DevBuf& w1 = scratch(s, 2);
     std::vector<int> ks_shape(in_shape, in_shape + ndim);
     ks_shape.insert(ks_shape.end(), out_shape, out_shape + ndim);
     std::vector<const double*> kf(factors, factors + (size_t)P * ndim);

@@ -1,6 +1,7 @@
 // Size-bucketed caching device allocator behind DevBuf (see internal.h).
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -51,12 +52,22 @@ void* pool_alloc(size_t bytes) {
   return p;
 }
 
-void pool_free(void* p, size_t bytes) {
+void pool_free(void* p, size_t bytes, int dev) {
   if (!p) return;
-  int dev = 0;
-  cudaGetDevice(&dev);
+  if (dev < 0) dev = current_device();
   std::lock_guard<std::mutex> lk(pool().mu);
   pool().free_blocks[{dev, round_bytes(bytes)}].push_back(p);
+}
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+DevBuf& scratch(cudaStream_t s, int slot) {
+  static thread_local std::map<std::tuple<int, cudaStream_t, int>, DevBuf> bufs;
+  return bufs[std::make_tuple(current_device(), s, slot)];
 }
 
 void pool_trim() {

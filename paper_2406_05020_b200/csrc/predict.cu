@@ -355,9 +355,12 @@ void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, do
   // repeats it — one slab covers config 1's 512 x 1024 grid on a B200
   size_t free_b = 0, total_b = 0;
   GPFVM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  // from the device size (deterministic slab plan), capped by what is free
-  const double budget = std::max(2e9, std::min({48e9, 0.3 * (double)total_b, 0.9 * (double)free_b}));
+  // from the device size (the same plan on every B200), then clamped to what
+  // is free (fewer rows per slab rather than an out-of-memory failure);
+  // GPFVM_PREDICT_SLAB_ROWS overrides (tests force the multi-slab path)
+  const double budget = std::min(std::min(48e9, 0.3 * (double)total_b), 0.9 * (double)free_b);
   int rows = (int)std::max<int64_t>(1, std::min<int64_t>(g.n[0], (int64_t)(budget / 8 / (4 * nbv * per_row))));
+  if (const char* e = getenv("GPFVM_PREDICT_SLAB_ROWS")) rows = std::max(1, std::min(g.n[0], atoi(e)));
   if (getenv("GPFVM_DEBUG"))
     fprintf(stderr, "[gpfvm] predict PRECOND: free %.1f GB, budget %.1f GB, %d rows per slab\n", free_b / 1e9,
             budget / 1e9, rows);

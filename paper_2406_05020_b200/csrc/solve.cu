@@ -167,6 +167,27 @@ static const KronTerm* find_term(gpfvm_problem* p, int I, int J, int fid0, int f
   return nullptr;
 }
 
+// The exact FD path needs G_PP to be exactly c_a A0 (x) A1 + c_b B0 (x) B1: two
+// Kronecker terms on the block, both diagonal pairs (a,a), (b,b).  When the R6
+// cross pair survives (even total derivative order, e.g. u_t + a u_x or the 1D
+// wave operator) a third term exists and FD would silently drop it.
+static bool exact_fd_ok(gpfvm_problem* p, int P) {
+  const BlockInt& B = p->blocks[P];
+  if (p->ndim != 2 || B.terms.size() != 2 || B.terms[0].output != B.terms[1].output) return false;
+  auto lookup = [&](int dim, int m) {
+    auto it = p->factor_index.find(FactorKey{B.terms[0].output, dim, P, m, P, m});
+    return it == p->factor_index.end() ? -1 : it->second;
+  };
+  int nPP = 0;
+  for (const auto& t : p->terms) nPP += (t.I == P && t.J == P);
+  if (nPP != 2) return false;
+  for (const auto& tm : B.terms) {
+    const int f0 = lookup(0, tm.order[0]), f1 = lookup(1, tm.order[1]);
+    if (f0 < 0 || f1 < 0 || !find_term(p, P, P, f0, f1)) return false;
+  }
+  return true;
+}
+
 static void build_fd(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   const BlockInt& B = p->blocks[pc.P];
   GPFVM_CHECK(p->ndim == 2 && B.terms.size() == 2, GPFVM_ERR_UNSUPPORTED,
@@ -600,10 +621,13 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
 
 static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
   if (p->pc && p->pc->type == type) return;
+  // validate before dropping the cached preconditioner (a failed request must
+  // not invalidate a later COV_PRECOND predict)
+  GPFVM_CHECK(type == GPFVM_PRECOND_NONE || type == GPFVM_PRECOND_BLOCK_FD, GPFVM_ERR_UNSUPPORTED,
+              "unsupported preconditioner");
   destroy_precond(p->pc);
   p->pc = nullptr;
   if (type == GPFVM_PRECOND_NONE) return;
-  GPFVM_CHECK(type == GPFVM_PRECOND_BLOCK_FD, GPFVM_ERR_UNSUPPORTED, "unsupported preconditioner");
   double t0 = now_ms();
   auto pc = new Precond();
   try {
@@ -621,9 +645,7 @@ static void build_precond(gpfvm_problem* p, int type, cudaStream_t s) {
     }
     // exact path: one 2D two-term PDE block + a dense IC/BC Schur
     // complement; otherwise block-Jacobi fast diagonalisation (§5.4)
-    const bool exact = nfree == 1 && p->ndim == 2 && p->blocks[pc->P].terms.size() == 2 &&
-                       p->blocks[pc->P].terms[0].output == p->blocks[pc->P].terms[1].output && nb <= 16384 &&
-                       getenv("GPFVM_FORCE_BJFD") == nullptr;
+    const bool exact = nfree == 1 && exact_fd_ok(p, pc->P) && nb <= 16384 && getenv("GPFVM_FORCE_BJFD") == nullptr;
     PhaseTimer pt(s);
     if (exact) {
       build_fd(p, *pc, s);

@@ -89,7 +89,7 @@ void dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, d
   // (e.g. the n_b-long rows of S^{-1}) do not launch 296 near-empty CTAs each;
   // fixed for a given n, hence still deterministic
   const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (n + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
-  static thread_local DevBuf partial;
+  DevBuf& partial = scratch(s, 0);
   partial.ensure((size_t)RED_BLOCKS * k);
   dot_partial_kernel<<<dim3(nblk, k), RED_THREADS, 0, s>>>(X, ldx, v, n, partial.ptr);
   dot_final_kernel<<<k, 512, 0, s>>>(partial.ptr, nblk, out);
