@@ -6,7 +6,7 @@ import scipy.linalg as sl
 
 import gpfvm_inputs as gi
 from gpfvm_inputs import Block, Kernel1D, Problem, Sites, Term
-from oracle.gram import KroneckerGram, dense_cross_cov, dense_gram, factor_matrix
+from oracle.gram import KroneckerGram, dense_cross_cov, dense_gram, factor_matrix, prior_variance
 from oracle.matern import matern_direct
 from oracle.posterior import posterior_exact, variance_itergp, variance_precond
 from oracle.solve import BlockLDLPreconditioner, FDPreconditioner, cholesky_solve, itergp_cg
@@ -267,3 +267,23 @@ def test_fvm_functional_tends_to_collocation():
         errs.append(np.abs(F - ref).max())
     assert errs[0] > errs[1] > errs[2]
     assert np.log2(errs[1] / errs[2]) > 1.5, errs
+
+
+def test_itergp_variance_full_budget_equals_exact():
+    """At full budget (N iterations, full reorthogonalisation) IterGP's
+    C_N = sum_j d_j d_j^T / eta_j is G^{-1} (its directions are a G-conjugate
+    basis of R^N; Wenger et al. via PAPER.md §4.1 l.299-302), so the combined
+    variance equals the exact posterior variance of Eq. 6 (l.114).  Dropping
+    the last direction leaves a visible computational-uncertainty gap."""
+    p = gi.heat_problem(4, 4)
+    G = dense_gram(p)
+    N = G.shape[0]
+    g = gi.heat_grid(7, 7)
+    _, vex, _ = posterior_exact(p, g, G, p.rhs())
+    tr = itergp_cg(lambda v: G @ v, p.rhs(), rtol=0.0, max_iter=N)
+    assert len(tr.etas) == N
+    v = variance_itergp(p, g, tr.directions, tr.etas)
+    prior = prior_variance(p, 0)
+    assert np.abs(v - vex).max() <= 1e-9 * prior
+    v_short = variance_itergp(p, g, tr.directions[:N - 4], tr.etas[:N - 4])
+    assert np.abs(v_short - vex).max() >= 1e-7 * prior
