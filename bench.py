@@ -144,6 +144,69 @@ def cpu_baseline(seconds: float = 15.0):
                       f"factor construction excluded"}
 
 
+def fp64_peak_live(gp):
+    """FP64 tensor-core roofline denominator measured in this run
+    (gpfvm_probe_fp64_peak: register-only DMMA.8x8x4 probe); MEASURED_PEAKS.json
+    has no FP64 entry."""
+    import ctypes as C
+    import torch
+    v = C.c_double(0.0)
+    rc = gp.lib.gpfvm_probe_fp64_peak(C.byref(v), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc == 0 and v.value > 1.0:
+        return v.value, ("live DMMA.8x8x4 probe in this run (gpfvm_probe_fp64_peak); MEASURED_PEAKS.json has no "
+                         "FP64 entry; tools/fp64_peak_bench: DMMA 37.0, cuBLAS DGEMM 35.4 (profiles/fp64_peak.txt)")
+    return 37.0, "tools/fp64_peak_bench DMMA.8x8x4 on this pool's B200 (profiles/fp64_peak.txt)"
+
+
+def _traffic():
+    """DRAM bytes (read + write) per matvec from the committed ncu capture
+    (profiles/r02_traffic.json, written by tools/ncu_traffic.py from a
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` pass over every
+    kernel of one matvec)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+    except Exception:
+        return {}
+
+
+def bench_config(builder, R, dev, peak, traffic, world):
+    """Matvec of a BASELINE 3D config (R right-hand sides resident in HBM):
+    graph replay timed with CUDA events over 5 launches after 3 warm-ups."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import gpfvm_inputs as gi
+    from paper_2406_05020_b200 import GpfvmProblem
+    p = builder()
+    gp = GpfvmProblem(p, device=dev.index or 0)
+    gp.gpfvm_assemble_factors()
+    N = gp.N
+    X = torch.tensor(gi.random_vectors(N, R, 7), dtype=torch.float64, device=dev)
+    Y = torch.empty_like(X)
+    for _ in range(3):
+        gp.gpfvm_gram_matvec(X, out=Y)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        gp.gpfvm_gram_matvec(X, out=Y)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    flops = gp.matvec_flops() * R
+    out = {"workload": p.name if hasattr(p, "name") else builder.__name__, "n_obs": int(N), "nrhs": R, "matvec_ms": ms,
+           "GB_s": world * 16.0 * N * R / (ms * 1e-3) / 1e9, "TFLOP_s": flops / (ms * 1e-3) / 1e12,
+           "frac": flops / (ms * 1e-3) / 1e12 / peak, "algorithmic_bytes": 16 * N * R,
+           "traffic": traffic.get("dram_bytes"), "traffic_source": traffic.get("source")}
+    del gp, X, Y
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -176,6 +239,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sharded", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -290,17 +354,23 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    fp64_peak = 37.0  # TFLOP/s, DMMA.8x8x4 microbenchmark on this pool's B200 (profiles/fp64_peak.txt)
+    fp64_peak, peak_src = fp64_peak_live(gp)
+    traffic = _traffic()
     achieved = flops_mv / (mv_ms_max * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs)",
+    roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs, whole matvec graph)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 entry",
-                "traffic": 0.866e9,
-                "traffic_note": "dram read+write of the two CUTLASS mode-product GEMMs of one 128-RHS matvec, "
-                                "ncu --set full (profiles/r01f_matvec_cutlass_full.txt): 348 MB + 518 MB vs "
-                                "270 MB algorithmic (X in, Y out) - the extra is the 268 MB intermediate Z "
-                                "written by stage 0 and read by stage 1",
-                "flops_per_launch": flops_mv}
+                "peak_source": peak_src,
+                "traffic": traffic.get("config1", {}).get("dram_bytes"),
+                "traffic_source": traffic.get("config1", {}).get("source"),
+                "algorithmic_bytes": bytes_mv, "flops_per_launch": flops_mv}
+    configs = None
+    if not args.no_configs:
+        configs = {}
+        for name, builder, nr in (("config2", gi.config2, 4), ("config3", gi.config3, 4), ("config4", gi.config4, 4)):
+            try:
+                configs[name] = bench_config(builder, nr, dev, fp64_peak, traffic.get(name, {}), world)
+            except Exception as e:  # never break the headline line
+                configs[name] = {"error": repr(e)[:200]}
 
     sharded = None
     if not args.no_sharded:
@@ -354,6 +424,7 @@ def main():
             "ms": {k: float(np.mean(v)) for k, v in times.items()},
             "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
             "clocks": clk.summary(), "hbm_peak_gbs": peaks.get("hbm_gbs"), "sharded": sharded,
+            "configs": configs,
         }
         print(json.dumps(line))
     if world > 1:

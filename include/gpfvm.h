@@ -264,6 +264,12 @@ int64_t gpfvm_launch_count(void);
  * term cancellation of DESIGN.md R6; low-rank and mode updates counted as
  * the GEMMs/streams actually run).  0 before assembly. */
 double gpfvm_matvec_flops(const gpfvm_problem* p);
+/* FP64 tensor-core peak probe (the roofline denominator bench.py reports):
+ * a register-only DMMA.8x8x4 (mma.sync.m8n8k4.f64) kernel, 4 CTAs x 8 warps
+ * per SM, each warp issuing 8 independent accumulator chains; best of two
+ * ~2 ms launches on `stream`, timed with CUDA events.  *tflops receives
+ * TFLOP/s (2 x 256 flops per DMMA).  Synchronises the stream. */
+int gpfvm_probe_fp64_peak(double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

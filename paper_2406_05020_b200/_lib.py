@@ -74,6 +74,7 @@ EXPORTS = {
     "gpfvm_kron_matvec": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double),
                                     C.POINTER(C.c_void_p), C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
                                     C.c_double, C.c_void_p]),
+    "gpfvm_probe_fp64_peak": (C.c_int, [C.POINTER(C.c_double), C.c_void_p]),
     "gpfvm_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                              C.c_double, C.c_void_p, C.c_int64, C.c_void_p]),
     "gpfvm_permute": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p, C.c_void_p,

@@ -2,6 +2,8 @@
 //   gpfvm_gemm     row-major DMMA GEMM (the time contraction after the all-to-all)
 //   gpfvm_permute  <=4D tensor permutation (layout changes around the all-to-all)
 //   gpfvm_sygv     generalised symmetric-definite eigensolver (FD factors)
+#include <algorithm>
+
 #include "problem.h"
 
 namespace gpfvm {
@@ -26,6 +28,25 @@ __global__ void permute_kernel(const double* __restrict__ src, double* __restric
   }
 }
 
+// register-only DMMA throughput probe (8 independent accumulator chains per warp)
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* out, int iters) {
+  const double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; i++) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += c[i][0] + c[i][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <class F>
 int guarded2(F&& f) {
   try {
@@ -43,6 +64,39 @@ int guarded2(F&& f) {
 }  // namespace gpfvm
 
 using namespace gpfvm;
+
+extern "C" int gpfvm_probe_fp64_peak(double* tflops, void* stream) {
+  return guarded2([&] {
+    GPFVM_CHECK(tflops, GPFVM_ERR_INVALID, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0, sms = 0;
+    GPFVM_CUDA(cudaGetDevice(&dev));
+    GPFVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = sms * 4, threads = 256, iters = 4096;
+    DevBuf out;
+    out.ensure((size_t)blocks * threads);
+    cudaEvent_t e0, e1;
+    GPFVM_CUDA(cudaEventCreate(&e0));
+    GPFVM_CUDA(cudaEventCreate(&e1));
+    dmma_probe_kernel<<<blocks, threads, 0, s>>>(out.ptr, 16);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 2; rep++) {
+      GPFVM_CUDA(cudaEventRecord(e0, s));
+      dmma_probe_kernel<<<blocks, threads, 0, s>>>(out.ptr, iters);
+      GPFVM_CUDA(cudaEventRecord(e1, s));
+      GPFVM_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      GPFVM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    count_launch(3);
+    check_launch("dmma_probe_kernel");
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 256 * 8 * (double)iters * blocks * (threads / 32);
+    *tflops = flops / (best * 1e-3) / 1e12;
+  });
+}
 
 extern "C" int gpfvm_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda, const double* B,
                           int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
