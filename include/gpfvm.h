@@ -222,6 +222,9 @@ typedef struct {
   double precond_shift;      /* Schur-complement shift used (0 normally) */
   double setup_ms;           /* preconditioner build (first call) */
   double iterate_ms;
+  int breakdown;             /* 1: stopped because eta_i = d_i^T G d_i <= 0 or non-finite
+                                (loss of positive definiteness in rounding); alpha and the
+                                kept actions are those of the completed iterations */
 } gpfvm_solve_report;
 
 int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_solve_opts* opts,

@@ -50,7 +50,7 @@ class SolveOpts(C.Structure):
 class SolveReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("rel_residual", C.c_double),
                 ("true_rel_residual", C.c_double), ("precond_shift", C.c_double),
-                ("setup_ms", C.c_double), ("iterate_ms", C.c_double)]
+                ("setup_ms", C.c_double), ("iterate_ms", C.c_double), ("breakdown", C.c_int)]
 
 
 class Grid(C.Structure):

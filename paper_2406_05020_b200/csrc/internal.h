@@ -149,6 +149,18 @@ void dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, d
               cudaStream_t s);  // out[j] = X_j . v   (j < k)
 void axpy_many(double* y, const double* X, int64_t ldx, const double* coef, double sign, int64_t n,
                int k, cudaStream_t s);  // y += sign * sum_j coef[j] X_j
+// IterGP/PCG iteration kernels with device-resident scalars: state[ST_*]
+enum { ST_NY = 0, ST_NR = 1, ST_THR = 2, ST_A = 3, ST_ETA = 4, ST_DONE = 5, ST_COUNT = 6, ST_SIZE = 8 };
+void itergp_init(const double* y, int64_t n, double rtol, double* state, cudaStream_t s);  // ||y||, flags
+// c_j = Kd_j . gd / eta_j (j < w)
+void itergp_reorth_coefs(const double* Kd, int64_t ld, int w, const double* gd, int64_t n, const double* eta,
+                         double* c, const double* state, cudaStream_t s);
+// dout = d - sum c_j Kd_j, gout = g - sum c_j Kg_j; eta = dout.gout -> *eta_slot, a = dout.r / eta
+void itergp_update(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
+                   const double* c, const double* r, double* dout, double* gout, int64_t n, double* state,
+                   double* eta_slot, cudaStream_t s);
+// x += a dn, r -= a gn, ||r|| -> state, convergence flag, iteration counter
+void itergp_step(double* x, double* r, const double* dn, const double* gn, int64_t n, double* state, cudaStream_t s);
 void fill(double* x, double v, int64_t n, cudaStream_t s);
 void copy(double* dst, const double* src, int64_t n, cudaStream_t s);
 void gather(double* dst, const double* src, const int64_t* idx, int64_t n, cudaStream_t s);

@@ -710,16 +710,17 @@ void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s)
   }
 }
 
-static void ensure_krylov(gpfvm_problem* p, int need, cudaStream_t s) {
+// grow the Krylov store to `need` slots, keeping the first `valid` ones
+static void ensure_krylov(gpfvm_problem* p, int need, int valid, cudaStream_t s) {
   Krylov& K = p->kry;
   if (need <= K.cap) return;
   int cap = std::max(need, std::max(8, K.cap * 2));
   DevBuf d, gd;
   d.ensure((size_t)cap * p->N);
   gd.ensure((size_t)cap * p->N);
-  if (K.k > 0) {
-    copy(d.ptr, K.d.ptr, (int64_t)K.k * p->N, s);
-    copy(gd.ptr, K.gd.ptr, (int64_t)K.k * p->N, s);
+  if (valid > 0) {
+    copy(d.ptr, K.d.ptr, (int64_t)valid * p->N, s);
+    copy(gd.ptr, K.gd.ptr, (int64_t)valid * p->N, s);
   }
   K.d = std::move(d);
   K.gd = std::move(gd);
@@ -746,36 +747,43 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
   Krylov& K = p->kry;
   K.k = 0;
   K.eta.clear();
-  DevBuf r, sc;
-  r.ensure(N);
-  sc.ensure(std::max(8, o.max_iter + 8));
-  double* dsc = sc.ptr;  // scalars
-  copy(r.ptr, y, N, s);
-  fill(x, 0.0, N, s);
-  const double ny = norm2(y, N, dsc, s);
-  double nr = ny;
-  int it = 0;
-  rep.converged = 0;
-  if (ny == 0.0) {
-    rep.converged = 1;
-  }
-  std::vector<double> coef;
   // keep_actions = 0: only a ring of W = max(1, reorth_window) actions is kept
   // (memory O(W N) for long budgeted solves); the IterGP covariance then
   // covers those W actions only
   const bool keep = o.keep_actions != 0;
   const int W = keep ? 0 : std::max(1, o.reorth_window);
-  int64_t total_it = 0;
-  while (!rep.converged && it < o.max_iter) {
-    if (nr <= o.rtol * ny) {
-      rep.converged = 1;
+  const int neta = keep ? std::max(1, o.max_iter) : W;
+  DevBuf r, sc;
+  r.ensure(N);
+  // device scalars: [state (ST_SIZE)] [c: reorthogonalisation coefficients] [eta_j]
+  sc.ensure((size_t)ST_SIZE + 2 * (size_t)neta + 8);
+  double* state = sc.ptr;
+  double* cdev = sc.ptr + ST_SIZE;
+  double* etad = cdev + neta;
+  copy(r.ptr, y, N, s);
+  fill(x, 0.0, N, s);
+  itergp_init(y, N, o.rtol, state, s);
+  // host view of the state: read only at the periodic checks (iterations 1-4,
+  // then every 4th) — the kernels themselves stop once converged
+  double hst[ST_SIZE];
+  auto read_state = [&]() {
+    GPFVM_CUDA(cudaMemcpyAsync(hst, state, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  };
+  read_state();
+  const double ny = hst[ST_NY];
+  int it = 0;  // host-issued iterations (>= the device count)
+  while (it < o.max_iter) {
+    if (it > 0 && (it <= 4 || it % 4 == 0)) {
+      read_state();
+      if (hst[ST_DONE] != 0.0) break;
+    } else if (it == 0 && hst[ST_DONE] != 0.0) {
       break;
     }
-    const int stored = keep ? K.k : (int)std::min<int64_t>(total_it, W);
-    const int slot = keep ? K.k : (int)(total_it % W);
-    ensure_krylov(p, keep ? K.k + 1 : std::min<int64_t>(total_it + 1, W), s);
-    // s = P^{-1} r ; z = G s  on fixed operands (graph-replayed matvec),
-    // G-orthogonalised there, then copied into the Krylov slot
+    const int stored = keep ? it : std::min(it, W);
+    const int slot = keep ? it : it % W;
+    ensure_krylov(p, keep ? it + 1 : std::min(it + 1, W), stored, s);
+    // s = P^{-1} r ; z = G s  on fixed operands (graph-replayed matvec)
     p->pcg_s.ensure(N);
     p->pcg_z.ensure(N);
     double* d = p->pcg_s.ptr;
@@ -783,59 +791,41 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
     if (p->pc) precond_apply(p, r.ptr, d, s);
     else copy(d, r.ptr, N, s);
     matvec_device(p, d, gd, 1, N, s);
-    if (stored > 0) {
-      // c_j = d_j . z / eta_j ; d -= sum c_j d_j ; gd -= sum c_j gd_j over the last
-      // `w` kept directions (w = k: full reorthogonalisation, §6 l.475; w = 1: the
-      // PCG recurrence, equivalent in exact arithmetic)
-      const int w = keep ? ((o.reorth_window > 0) ? std::min(o.reorth_window, stored) : stored) : stored;
-      const int j0 = stored - w;
-      dot_many(K.d.ptr + (int64_t)j0 * N, N, gd, N, w, dsc, s);
-      coef.resize(w);
-      GPFVM_CUDA(cudaMemcpyAsync(coef.data(), dsc, sizeof(double) * w, cudaMemcpyDeviceToHost, s));
-      GPFVM_CUDA(cudaStreamSynchronize(s));
-      for (int j = 0; j < w; j++) coef[j] /= K.eta[j0 + j];
-      GPFVM_CUDA(cudaMemcpyAsync(dsc, coef.data(), sizeof(double) * w, cudaMemcpyHostToDevice, s));
-      axpy_many(d, K.d.ptr + (int64_t)j0 * N, N, dsc, -1.0, N, w, s);
-      axpy_many(gd, K.gd.ptr + (int64_t)j0 * N, N, dsc, -1.0, N, w, s);
-    }
-    // eta = Gd . d ; a = d . r / eta
-    dot_many(d, N, gd, N, 1, dsc, s);
-    dot_many(d, N, r.ptr, N, 1, dsc + 1, s);
-    double hs[2];
-    GPFVM_CUDA(cudaMemcpyAsync(hs, dsc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    GPFVM_CUDA(cudaStreamSynchronize(s));
-    const double eta = hs[0];
-    if (!(eta > 0.0) || !std::isfinite(eta)) break;  // breakdown: keep the trace so far
-    const double a = hs[1] / eta;
-    double ha[2] = {a, -a};
-    GPFVM_CUDA(cudaMemcpyAsync(dsc, ha, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
-    axpy_many(x, d, N, dsc, 1.0, N, 1, s);
-    axpy_many(r.ptr, gd, N, dsc + 1, 1.0, N, 1, s);
-    copy(K.d.ptr + (int64_t)slot * N, d, N, s);
-    copy(K.gd.ptr + (int64_t)slot * N, gd, N, s);
-    if (keep) {
-      K.eta.push_back(eta);
-      K.k++;
-    } else {
-      if ((int)K.eta.size() < W) K.eta.resize(W, 0.0);
-      K.eta[slot] = eta;
-      K.k = (int)std::min<int64_t>(total_it + 1, W);
-    }
-    total_it++;
+    // G-orthogonalise against the last w kept directions (w = k: full
+    // reorthogonalisation, §6 l.475; w = 1: the PCG recurrence), store the
+    // action in its Krylov slot, eta = d.Gd, a = d.r / eta: two fused passes
+    const int w = stored == 0 ? 0 : (keep && o.reorth_window > 0 ? std::min(o.reorth_window, stored) : stored);
+    const int j0 = stored - w;
+    itergp_reorth_coefs(K.d.ptr + (int64_t)j0 * N, N, w, gd, N, etad + j0, cdev, state, s);
+    double* dslot = K.d.ptr + (int64_t)slot * N;
+    double* gslot = K.gd.ptr + (int64_t)slot * N;
+    itergp_update(d, gd, K.d.ptr + (int64_t)j0 * N, K.gd.ptr + (int64_t)j0 * N, N, w, cdev, r.ptr, dslot, gslot, N,
+                  state, etad + slot, s);
+    itergp_step(x, r.ptr, dslot, gslot, N, state, s);
     it++;
-    nr = norm2(r.ptr, N, dsc, s);
   }
-  if (!keep && (int)K.eta.size() > K.k) K.eta.resize(K.k);
-  if (!rep.converged && nr <= o.rtol * ny) rep.converged = 1;
-  rep.iterations = it;
+  read_state();
+  const int done_it = (int)hst[ST_COUNT];
+  const bool breakdown = hst[ST_DONE] == 2.0;
+  // the kept actions: every completed iteration (ring: the last min(done, W))
+  K.k = keep ? done_it : std::min(done_it, W);
+  K.eta.assign(K.k, 0.0);
+  if (K.k > 0) {
+    GPFVM_CUDA(cudaMemcpyAsync(K.eta.data(), etad, sizeof(double) * K.k, cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  }
+  const double nr = hst[ST_NR];
+  rep.converged = (hst[ST_DONE] == 1.0 || (ny > 0 && nr <= o.rtol * ny) || ny == 0.0) ? 1 : 0;
+  rep.breakdown = breakdown ? 1 : 0;
+  rep.iterations = done_it;
   rep.rel_residual = ny > 0 ? nr / ny : 0.0;
   rep.iterate_ms = now_ms() - t0;
-  // true residual
+  // true residual ||G x - y||
   matvec_device(p, x, r.ptr, 1, N, s);
   double one = 1.0;
-  GPFVM_CUDA(cudaMemcpyAsync(dsc, &one, sizeof(double), cudaMemcpyHostToDevice, s));
-  axpy_many(r.ptr, y, N, dsc, -1.0, N, 1, s);  // r = Gx - y
-  double tr = norm2(r.ptr, N, dsc + 1, s);
+  GPFVM_CUDA(cudaMemcpyAsync(cdev, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  axpy_many(r.ptr, y, N, cdev, -1.0, N, 1, s);  // r = Gx - y
+  double tr = norm2(r.ptr, N, cdev + 1, s);
   rep.true_rel_residual = ny > 0 ? tr / ny : 0.0;
 }
 

@@ -77,24 +77,200 @@ __global__ void scatter_kernel(double* __restrict__ dst, const double* __restric
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[idx[i]] = src[i];
 }
 
+// ---- IterGP/PCG iteration with device-resident scalars ----
+// state[ST_*] lives in device memory; every kernel returns immediately once
+// state[ST_DONE] != 0, so the host only has to look at the state every few
+// iterations (no per-iteration host synchronisation).
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[32];
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = (threadIdx.x < (blockDim.x >> 5)) ? ws[threadIdx.x] : 0.0;
+  if (threadIdx.x < 32) t = warp_sum(t);
+  return t;  // valid in thread 0
+}
+
+// c_j = (Kd_j . gd) / eta_j   (final pass of the reorthogonalisation dots)
+__global__ void reorth_final_kernel(const double* __restrict__ partial, int nparts, const double* __restrict__ eta,
+                                    double* __restrict__ c, const double* __restrict__ state) {
+  if (state[ST_DONE] != 0.0) return;
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[(int64_t)j * nparts + i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) c[j] = s / eta[j];
+}
+
+// d' = d - sum_j c_j Kd_j ; g' = g - sum_j c_j Kg_j (written to the Krylov slot);
+// partial sums of d'.g' and d'.r
+__global__ void __launch_bounds__(RED_THREADS) itergp_update_kernel(
+    const double* __restrict__ d, const double* __restrict__ g, const double* __restrict__ Kd,
+    const double* __restrict__ Kg, int64_t ld, int w, const double* __restrict__ c, const double* __restrict__ r,
+    double* __restrict__ dout, double* __restrict__ gout, int64_t n, double* __restrict__ partial,
+    const double* __restrict__ state) {
+  if (state[ST_DONE] != 0.0) return;
+  double s_eta = 0.0, s_del = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    // projection first, then one subtraction (the rounding of axpy_many)
+    double pd = 0.0, pg = 0.0;
+    for (int j = 0; j < w; j++) {
+      const double cj = c[j];
+      pd = fma(cj, Kd[j * ld + i], pd);
+      pg = fma(cj, Kg[j * ld + i], pg);
+    }
+    const double dv = d[i] - pd, gv = g[i] - pg;
+    dout[i] = dv;
+    gout[i] = gv;
+    s_eta = fma(dv, gv, s_eta);
+    s_del = fma(dv, r[i], s_del);
+  }
+  s_eta = block_sum(s_eta);
+  s_del = block_sum(s_del);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = s_eta;
+    partial[gridDim.x + blockIdx.x] = s_del;
+  }
+}
+
+// eta = d'.g', a = d'.r / eta; breakdown (eta <= 0 or not finite) stops the iteration
+__global__ void itergp_update_final_kernel(const double* __restrict__ partial, int nparts, double* __restrict__ state,
+                                           double* __restrict__ eta_slot) {
+  if (state[ST_DONE] != 0.0) return;
+  double se = 0.0, sd = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+    se += partial[i];
+    sd += partial[nparts + i];
+  }
+  se = block_sum(se);
+  sd = block_sum(sd);
+  if (threadIdx.x == 0) {
+    if (!(se > 0.0) || !isfinite(se) || !isfinite(sd)) {
+      state[ST_DONE] = 2.0;  // breakdown: the trace so far is kept
+      return;
+    }
+    *eta_slot = se;
+    state[ST_ETA] = se;
+    state[ST_A] = sd / se;
+  }
+}
+
+// x += a d', r -= a g', partial sums of r.r
+__global__ void __launch_bounds__(RED_THREADS) itergp_step_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                                  const double* __restrict__ dn,
+                                                                  const double* __restrict__ gn, int64_t n,
+                                                                  double* __restrict__ partial,
+                                                                  const double* __restrict__ state) {
+  if (state[ST_DONE] != 0.0) return;
+  const double a = state[ST_A];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(a, dn[i], x[i]);
+    const double rv = fma(-a, gn[i], r[i]);
+    r[i] = rv;
+    s = fma(rv, rv, s);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// ||r||, convergence flag, iteration counter
+__global__ void itergp_step_final_kernel(const double* __restrict__ partial, int nparts, double* __restrict__ state) {
+  if (state[ST_DONE] != 0.0) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) {
+    const double nr = sqrt(s);
+    state[ST_NR] = nr;
+    state[ST_COUNT] += 1.0;
+    if (nr <= state[ST_THR]) state[ST_DONE] = 1.0;
+  }
+}
+
+// ||y|| and the initial state
+__global__ void itergp_init_kernel(const double* __restrict__ partial, int nparts, double rtol, double* __restrict__ state) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[i];
+  s = block_sum(s);
+  if (threadIdx.x == 0) {
+    const double ny = sqrt(s);
+    state[ST_NY] = ny;
+    state[ST_NR] = ny;
+    state[ST_THR] = rtol * ny;
+    state[ST_COUNT] = 0.0;
+    state[ST_A] = state[ST_ETA] = 0.0;
+    state[ST_DONE] = (ny == 0.0 || ny <= rtol * ny) ? 1.0 : 0.0;
+  }
+}
+
 unsigned grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8));
 }
 }  // namespace
 
+int red_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (n + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
+}
+
 void dot_many(const double* X, int64_t ldx, const double* v, int64_t n, int k, double* out, cudaStream_t s) {
   if (k <= 0) return;
   // blocks per dot from the length (>= 4 elements per thread), so short dots
   // (e.g. the n_b-long rows of S^{-1}) do not launch 296 near-empty CTAs each;
   // fixed for a given n, hence still deterministic
-  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (n + 4 * RED_THREADS - 1) / (4 * RED_THREADS)));
+  const int nblk = red_blocks(n);
   DevBuf& partial = scratch(s, 0);
   partial.ensure((size_t)RED_BLOCKS * k);
   dot_partial_kernel<<<dim3(nblk, k), RED_THREADS, 0, s>>>(X, ldx, v, n, partial.ptr);
   dot_final_kernel<<<k, 512, 0, s>>>(partial.ptr, nblk, out);
   count_launch(2);
   check_launch("dot_many");
+}
+
+void itergp_init(const double* y, int64_t n, double rtol, double* state, cudaStream_t s) {
+  const int nblk = red_blocks(n);
+  DevBuf& partial = scratch(s, 3);
+  partial.ensure((size_t)2 * RED_BLOCKS);
+  dot_partial_kernel<<<dim3(nblk, 1), RED_THREADS, 0, s>>>(y, n, y, n, partial.ptr);
+  itergp_init_kernel<<<1, 256, 0, s>>>(partial.ptr, nblk, rtol, state);
+  count_launch(2);
+  check_launch("itergp_init");
+}
+
+void itergp_reorth_coefs(const double* Kd, int64_t ld, int w, const double* gd, int64_t n, const double* eta,
+                         double* c, const double* state, cudaStream_t s) {
+  if (w <= 0) return;
+  const int nblk = red_blocks(n);
+  DevBuf& partial = scratch(s, 4);
+  partial.ensure((size_t)RED_BLOCKS * w);
+  dot_partial_kernel<<<dim3(nblk, w), RED_THREADS, 0, s>>>(Kd, ld, gd, n, partial.ptr);
+  reorth_final_kernel<<<w, 256, 0, s>>>(partial.ptr, nblk, eta, c, state);
+  count_launch(2);
+  check_launch("itergp_reorth_coefs");
+}
+
+void itergp_update(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
+                   const double* c, const double* r, double* dout, double* gout, int64_t n, double* state,
+                   double* eta_slot, cudaStream_t s) {
+  const int nblk = red_blocks(n);
+  DevBuf& partial = scratch(s, 3);
+  partial.ensure((size_t)2 * RED_BLOCKS);
+  itergp_update_kernel<<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
+  itergp_update_final_kernel<<<1, 256, 0, s>>>(partial.ptr, nblk, state, eta_slot);
+  count_launch(2);
+  check_launch("itergp_update");
+}
+
+void itergp_step(double* x, double* r, const double* dn, const double* gn, int64_t n, double* state, cudaStream_t s) {
+  const int nblk = red_blocks(n);
+  DevBuf& partial = scratch(s, 3);
+  partial.ensure((size_t)2 * RED_BLOCKS);
+  itergp_step_kernel<<<nblk, RED_THREADS, 0, s>>>(x, r, dn, gn, n, partial.ptr, state);
+  itergp_step_final_kernel<<<1, 256, 0, s>>>(partial.ptr, nblk, state);
+  count_launch(2);
+  check_launch("itergp_step");
 }
 
 void axpy_many(double* y, const double* X, int64_t ldx, const double* coef, double sign, int64_t n, int k,
