@@ -104,7 +104,11 @@ __global__ void reorth_final_kernel(const double* __restrict__ partial, int npar
 }
 
 // d' = d - sum_j c_j Kd_j ; g' = g - sum_j c_j Kg_j (written to the Krylov slot);
-// partial sums of d'.g' and d'.r
+// partial sums of d'.g' and d'.r.  HBM-bound on the 2 w N reads of the kept
+// actions: two consecutive elements per thread (16-byte loads) and four
+// actions per step keep 16 loads in flight per thread (n, ld even, 16-byte
+// aligned pointers: checked by the host wrapper; a scalar variant otherwise).
+template <bool V2>
 __global__ void __launch_bounds__(RED_THREADS) itergp_update_kernel(
     const double* __restrict__ d, const double* __restrict__ g, const double* __restrict__ Kd,
     const double* __restrict__ Kg, int64_t ld, int w, const double* __restrict__ c, const double* __restrict__ r,
@@ -112,19 +116,55 @@ __global__ void __launch_bounds__(RED_THREADS) itergp_update_kernel(
     const double* __restrict__ state) {
   if (state[ST_DONE] != 0.0) return;
   double s_eta = 0.0, s_del = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    // projection first, then one subtraction (the rounding of axpy_many)
-    double pd = 0.0, pg = 0.0;
-    for (int j = 0; j < w; j++) {
-      const double cj = c[j];
-      pd = fma(cj, Kd[j * ld + i], pd);
-      pg = fma(cj, Kg[j * ld + i], pg);
+  if (V2) {
+    const int64_t n2 = n >> 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+      // projection first, then one subtraction (the rounding of axpy_many)
+      double2 pd = make_double2(0.0, 0.0), pg = make_double2(0.0, 0.0);
+      int j = 0;
+      for (; j + 4 <= w; j += 4) {
+        double2 kd[4], kg[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          kd[u] = __ldcs(reinterpret_cast<const double2*>(Kd + (j + u) * ld) + i);
+          kg[u] = __ldcs(reinterpret_cast<const double2*>(Kg + (j + u) * ld) + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const double cj = c[j + u];
+          pd.x = fma(cj, kd[u].x, pd.x); pd.y = fma(cj, kd[u].y, pd.y);
+          pg.x = fma(cj, kg[u].x, pg.x); pg.y = fma(cj, kg[u].y, pg.y);
+        }
+      }
+      for (; j < w; j++) {
+        const double cj = c[j];
+        const double2 kd = __ldcs(reinterpret_cast<const double2*>(Kd + j * ld) + i);
+        const double2 kg = __ldcs(reinterpret_cast<const double2*>(Kg + j * ld) + i);
+        pd.x = fma(cj, kd.x, pd.x); pd.y = fma(cj, kd.y, pd.y);
+        pg.x = fma(cj, kg.x, pg.x); pg.y = fma(cj, kg.y, pg.y);
+      }
+      const double2 dv2 = reinterpret_cast<const double2*>(d)[i], gv2 = reinterpret_cast<const double2*>(g)[i];
+      const double2 rv = reinterpret_cast<const double2*>(r)[i];
+      const double2 dn = make_double2(dv2.x - pd.x, dv2.y - pd.y), gn = make_double2(gv2.x - pg.x, gv2.y - pg.y);
+      reinterpret_cast<double2*>(dout)[i] = dn;
+      reinterpret_cast<double2*>(gout)[i] = gn;
+      s_eta = fma(dn.x, gn.x, s_eta); s_eta = fma(dn.y, gn.y, s_eta);
+      s_del = fma(dn.x, rv.x, s_del); s_del = fma(dn.y, rv.y, s_del);
     }
-    const double dv = d[i] - pd, gv = g[i] - pg;
-    dout[i] = dv;
-    gout[i] = gv;
-    s_eta = fma(dv, gv, s_eta);
-    s_del = fma(dv, r[i], s_del);
+  } else {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      double pd = 0.0, pg = 0.0;
+      for (int j = 0; j < w; j++) {
+        const double cj = c[j];
+        pd = fma(cj, Kd[j * ld + i], pd);
+        pg = fma(cj, Kg[j * ld + i], pg);
+      }
+      const double dv = d[i] - pd, gv = g[i] - pg;
+      dout[i] = dv;
+      gout[i] = gv;
+      s_eta = fma(dv, gv, s_eta);
+      s_del = fma(dv, r[i], s_del);
+    }
   }
   s_eta = block_sum(s_eta);
   s_del = block_sum(s_del);
@@ -254,10 +294,18 @@ void itergp_reorth_coefs(const double* Kd, int64_t ld, int w, const double* gd, 
 void itergp_update(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
                    const double* c, const double* r, double* dout, double* gout, int64_t n, double* state,
                    double* eta_slot, cudaStream_t s) {
-  const int nblk = red_blocks(n);
-  DevBuf& partial = scratch(s, 3);
-  partial.ensure((size_t)2 * RED_BLOCKS);
-  itergp_update_kernel<<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool v2 = (n % 2 == 0) && (ld % 2 == 0) && a16(d) && a16(g) && a16(Kd) && a16(Kg) && a16(r) && a16(dout) &&
+                  a16(gout);
+  // enough CTAs to keep 2 w N streaming loads in flight (8 per SM), fixed for
+  // a given n so the reduction order (and the scalars) stay deterministic
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n / (v2 ? 2 : 1) + RED_THREADS - 1) / RED_THREADS));
+  DevBuf& partial = scratch(s, 5);
+  partial.ensure((size_t)2 * 148 * 8);
+  if (v2)
+    itergp_update_kernel<true><<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
+  else
+    itergp_update_kernel<false><<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
   itergp_update_final_kernel<<<1, 256, 0, s>>>(partial.ptr, nblk, state, eta_slot);
   count_launch(2);
   check_launch("itergp_update");
