@@ -169,7 +169,7 @@ def _traffic():
         return {}
 
 
-def bench_config(builder, R, dev, peak, traffic, world):
+def bench_config(builder, R, dev, peak, traffic, world, solve_budget=0):
     """Matvec of a BASELINE 3D config (R right-hand sides resident in HBM):
     graph replay timed with CUDA events over 5 launches after 3 warm-ups."""
     import numpy as np
@@ -202,6 +202,22 @@ def bench_config(builder, R, dev, peak, traffic, world):
            "GB_s": world * 16.0 * N * R / (ms * 1e-3) / 1e9, "TFLOP_s": flops / (ms * 1e-3) / 1e12,
            "frac": flops / (ms * 1e-3) / 1e12 / peak, "algorithmic_bytes": 16 * N * R,
            "traffic": traffic.get("dram_bytes"), "traffic_source": traffic.get("source")}
+    if solve_budget > 0:
+        # the paper's fixed IterGP budget for its 3D problem (P:l.444: 1250
+        # iterations), full reorthogonalisation, every action kept (P:l.475)
+        y = torch.tensor(p.rhs(), dtype=torch.float64, device=dev)
+        alpha = torch.empty_like(y)
+        gp.gpfvm_solve(y, rtol=1e-8, max_iter=2, out=alpha)  # preconditioner build, warm-up
+        torch.cuda.synchronize()
+        e0.record()
+        _, rep = gp.gpfvm_solve(y, rtol=1e-8, max_iter=solve_budget, out=alpha, reorth_window=0, keep_actions=True)
+        e1.record()
+        torch.cuda.synchronize()
+        out["solve"] = {"budget": solve_budget, "iterations": rep["iterations"], "converged": bool(rep["converged"]),
+                        "rel_residual": rep["rel_residual"], "true_rel_residual": rep["true_rel_residual"],
+                        "solve_s": e0.elapsed_time(e1) / 1e3, "reorth": "full", "actions_kept": rep["iterations"],
+                        "precond": "block-Jacobi FD (DESIGN.md 5.4)"}
+        del y, alpha
     del gp, X, Y
     torch.cuda.empty_cache()
     return out
@@ -240,6 +256,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sharded", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-budget-solve", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -368,7 +385,8 @@ def main():
         configs = {}
         for name, builder, nr in (("config2", gi.config2, 4), ("config3", gi.config3, 4), ("config4", gi.config4, 4)):
             try:
-                configs[name] = bench_config(builder, nr, dev, fp64_peak, traffic.get(name, {}), world)
+                configs[name] = bench_config(builder, nr, dev, fp64_peak, traffic.get(name, {}), world,
+                                             solve_budget=1250 if (name == "config2" and not args.no_budget_solve) else 0)
             except Exception as e:  # never break the headline line
                 configs[name] = {"error": repr(e)[:200]}
 
