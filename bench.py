@@ -223,6 +223,60 @@ def bench_config(builder, R, dev, peak, traffic, world, solve_budget=0):
     return out
 
 
+def bench_sharded(builder, dev, world, iters=20):
+    """Sharded matvec and IterGP iterations of a full BASELINE 3D problem over
+    the ranks of this job (max over ranks of CUDA-event times)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import gpfvm_inputs as gi
+    from paper_2406_05020_b200 import GpfvmProblem
+    from paper_2406_05020_b200.dist import ShardedProblem, TorchComm
+    p = builder()
+    gp = GpfvmProblem(p, device=dev.index or 0)
+    gp.gpfvm_assemble_factors()
+    sp = ShardedProblem([gp], TorchComm())
+    x = torch.tensor(gi.random_vectors(p.size, 1, 5)[0], dtype=torch.float64, device=dev)
+    xl = sp.local([x])
+    for _ in range(3):
+        sp.matvec(xl)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        sp.matvec(xl)
+    e1.record()
+    torch.cuda.synchronize()
+    mv = e0.elapsed_time(e1) / 5
+    y = torch.tensor(p.rhs(), dtype=torch.float64, device=dev)
+    yl = sp.local([y])
+    sp.solve(yl, rtol=0.0, max_iter=2, reorth_window=1)  # preconditioner build + warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record()
+    _, rep = sp.solve(yl, rtol=0.0, max_iter=iters, reorth_window=1)
+    e1.record()
+    torch.cuda.synchronize()
+    it_ms = e0.elapsed_time(e1) / max(1, iters)
+    t = torch.tensor([mv, it_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mv, it_ms = t.tolist()
+    cnt = sp.G.counts[0]
+    comm = int(sum(cnt[0][0]) - cnt[0][0][sp.comm.ranks[0]] + sum(cnt[2][0]) - cnt[2][0][sp.comm.ranks[0]]) * 8
+    out = {"workload": p.name, "ranks": world, "n_obs": int(p.size), "matvec_ms": mv,
+           "GB_s": 16.0 * p.size / (mv * 1e-3) / 1e9, "iteration_ms": it_ms, "iterations_timed": rep.iterations,
+           "precond": "sharded block-Jacobi FD", "bytes_sent_per_rank_per_matvec": comm,
+           "scaling": "strong (fixed problem split over the ranks)"}
+    sp.close()
+    del gp
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -392,39 +446,15 @@ def main():
 
     sharded = None
     if not args.no_sharded:
-        # time-sharded PDE-block operator of BASELINE config 3 (8.4M obs): NCCL all-to-all
-        # re-partition + one K-concatenated time GEMM per matvec
-        try:
-            from paper_2406_05020_b200.dist import GpuOps, ShardedKron, block_kron_terms
-            p3 = gi.config3()
-            P3 = len(p3.blocks) - 1
-            ops = GpuOps(dev)
-            coefs, facs = block_kron_terms(p3, P3, local)
-            shape = p3.blocks[P3].shape
-            A = ShardedKron(ops, shape, coefs, facs, None, rank, world)
-            nloc = (shape[0] // world) * shape[1] * shape[2]
-            xs = torch.randn(nloc, dtype=torch.float64, device=dev)
-            for _ in range(2):
-                A.matvec(xs)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            e0, e1 = ev(), ev()
-            e0.record()
-            for _ in range(5):
-                A.matvec(xs)
-            e1.record()
-            torch.cuda.synchronize()
-            tt = torch.tensor([e0.elapsed_time(e1) / 5], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            npde = shape[0] * shape[1] * shape[2]
-            sharded = {"workload": "config3 PDE block (time-sharded)", "ranks": world, "n_obs": int(npde),
-                       "ms": float(tt.item()),
-                       "GB_s": npde * 16 / (tt.item() * 1e-3) / 1e9, "terms": len(coefs),
-                       "comm_bytes_per_matvec": (len(coefs) + 1) * npde * 8}
-        except Exception as e:  # never break the headline line
-            sharded = {"error": repr(e)[:200]}
+        # time-sharded full problems (every block: IC planes on rank 0, faces and
+        # PDE block split along time; library gpfvm_shard_* + NCCL all_to_all,
+        # DESIGN.md §7): strong scaling of the matvec and of IterGP iterations
+        sharded = {}
+        for name, builder in (("config3", gi.config3), ("config4", gi.config4)):
+            try:
+                sharded[name] = bench_sharded(builder, dev, world)
+            except Exception as e:  # never break the headline line
+                sharded[name] = {"error": repr(e)[:200]}
     if rank == 0:
         cb = None
         if not args.no_cpu_baseline and world == 1:

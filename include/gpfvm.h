@@ -259,6 +259,78 @@ typedef struct {
 int gpfvm_predict(gpfvm_problem* p, const gpfvm_grid* grid, const double* alpha, double* mean,
                   double* var, int cov_mode, void* stream);
 
+/* ---- time-mode sharded operators (multi-GPU) ---------------
+ * north_star: "the observation tensor is sharded along the time mode; NCCL
+ * all-to-all re-partition for the time-mode contraction and an allreduce for
+ * the CG inner products".  Every block whose dimension 0 is the common time
+ * axis (n0 sites) is split into `world` contiguous time slabs (rank r owns
+ * sites [r n0/world, (r+1) n0/world)); blocks with one time site (IC planes)
+ * live on rank 0.  The local vector is the concatenation, block by block, of
+ * the owned rows (row-major, dimension 0 slowest); gpfvm_shard_layout gives
+ * the offsets.  One application of a sharded operator is three library calls
+ * around two all-to-all exchanges done by the caller (NCCL
+ * all_to_all_single with the per-rank counts of gpfvm_shard_counts):
+ *   begin(x_local) -> send1  | all-to-all | mid(recv1) -> send2 |
+ *   all-to-all | end(recv2) -> y_local.
+ * GPFVM_SHARD_GRAM: y = G x (Eq. 20, noise included), one phase (0).
+ * GPFVM_SHARD_PRECOND: block-Jacobi FD as phase 0 (Q^T),
+ * gpfvm_shard_precond_scale (D^{-1}, local) and phase 1 (Q).
+ * Every buffer is a device pointer owned by the caller; the handle owns its
+ * workspaces and must be destroyed before the problem.  Errors:
+ * GPFVM_ERR_STATE before assembly, GPFVM_ERR_UNSUPPORTED for d < 2 or blocks
+ * whose time extent is neither n0 nor 1, GPFVM_ERR_INVALID for bad ranks. */
+enum { GPFVM_SHARD_GRAM = 0, GPFVM_SHARD_PRECOND = 1 };
+typedef struct gpfvm_shard gpfvm_shard;
+int gpfvm_shard_create(gpfvm_problem* p, int rank, int world, int kind, gpfvm_shard** out, void* stream);
+int gpfvm_shard_destroy(gpfvm_shard* sh);
+/* local vector length on this rank */
+int64_t gpfvm_shard_local_size(const gpfvm_shard* sh);
+/* per block: offset in the local vector, first owned time row, owned rows,
+ * spatial size (arrays of n_blocks entries; any may be NULL) */
+int gpfvm_shard_layout(const gpfvm_shard* sh, int64_t* local_offset, int64_t* row0, int64_t* rows, int64_t* spatial);
+/* element counts per peer rank (arrays of `world` entries) of the two exchanges */
+int gpfvm_shard_counts(const gpfvm_shard* sh, int phase, int64_t* send1, int64_t* recv1, int64_t* send2,
+                       int64_t* recv2);
+int gpfvm_shard_apply_begin(gpfvm_shard* sh, int phase, const double* x_local, double* send1, void* stream);
+int gpfvm_shard_apply_mid(gpfvm_shard* sh, int phase, const double* recv1, double* send2, void* stream);
+/* y_local = (Gram: noise x_local; precond: 0) + the received contributions */
+int gpfvm_shard_apply_end(gpfvm_shard* sh, int phase, const double* recv2, const double* x_local, double* y_local,
+                          void* stream);
+int gpfvm_shard_precond_scale(gpfvm_shard* sh, double* z_local, void* stream);
+/* Host-only plan query (no device work; valid before assembly): the local
+ * length and the Gram's exchange counts of `rank` — the layout logic of
+ * gpfvm_shard_create, testable without a GPU. */
+int gpfvm_shard_plan_counts(const gpfvm_problem* p, int rank, int world, int64_t* local_n, int64_t* send1,
+                            int64_t* recv1, int64_t* send2, int64_t* recv2);
+/* the local slab of a full (block-concatenated, length N) device vector */
+int gpfvm_shard_gather_local(const gpfvm_shard* sh, const double* full, double* local, void* stream);
+
+/* ---- IterGP iteration steps with device-resident scalars (sharded solve) ---
+ * The single-GPU gpfvm_solve fuses these; the sharded solve (dist.py) calls
+ * them on local slabs and all_reduces (sum) the small `partial` arrays in
+ * between — the only arithmetic outside the library is that sum.
+ * state: GPFVM_ITER_STATE doubles (||y||, ||r||, threshold, a, eta, done flag
+ * (0 running, 1 converged, 2 breakdown), iteration count); once done != 0
+ * every step is a no-op.  Reference: PAPER.md §4.1 l.295-302 (IterGP, CG
+ * policy), §6 l.475 (full reorthogonalisation). */
+enum { GPFVM_ITER_STATE = 8 };
+/* state from ||y||^2 (the all-reduced local dot of y) */
+int gpfvm_iter_init(const double* yy, double rtol, double* state, void* stream);
+/* c_j = dots[j] / eta[j]  (dots: all-reduced K_d[j] . G d, j < w) */
+int gpfvm_iter_coefs(const double* dots, int w, const double* eta, double* c, const double* state, void* stream);
+/* d' = d - sum c_j Kd_j, g' = g - sum c_j Kg_j into dout/gout; partial[0..1] =
+ * local d'.g', d'.r */
+int gpfvm_iter_update_local(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
+                            const double* c, const double* r, double* dout, double* gout, int64_t n, double* partial,
+                            const double* state, void* stream);
+/* eta = sums[0] -> *eta_slot, a = sums[1] / eta (breakdown flag if eta <= 0) */
+int gpfvm_iter_update_final(const double* sums, double* state, double* eta_slot, void* stream);
+/* x += a dn, r -= a gn; partial[0] = local r.r */
+int gpfvm_iter_step_local(double* x, double* r, const double* dn, const double* gn, int64_t n, double* partial,
+                          const double* state, void* stream);
+/* ||r|| = sqrt(sum[0]), convergence flag, iteration count */
+int gpfvm_iter_step_final(const double* sum, double* state, void* stream);
+
 /* ---- instrumentation ------------------------------------------------------
  * Kernel-launch counter: every kernel this library launches increments it
  * (a replayed matvec graph counts its kernel nodes). */

@@ -86,6 +86,26 @@ EXPORTS = {
     "gpfvm_fd_setup": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                  C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_vmul": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "gpfvm_shard_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.c_void_p]),
+    "gpfvm_shard_destroy": (C.c_int, [C.c_void_p]),
+    "gpfvm_shard_local_size": (C.c_int64, [C.c_void_p]),
+    "gpfvm_shard_layout": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int64)] * 4),
+    "gpfvm_shard_counts": (C.c_int, [C.c_void_p, C.c_int] + [C.POINTER(C.c_int64)] * 4),
+    "gpfvm_shard_apply_begin": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_shard_apply_mid": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_shard_apply_end": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_shard_precond_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_shard_plan_counts": (C.c_int, [C.c_void_p, C.c_int, C.c_int] + [C.POINTER(C.c_int64)] * 5),
+    "gpfvm_shard_gather_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_init": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_coefs": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_update_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_update_final": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_step_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]),
+    "gpfvm_iter_step_final": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_launch_count": (C.c_int64, []),
     "gpfvm_matvec_flops": (C.c_double, [C.c_void_p]),
 }

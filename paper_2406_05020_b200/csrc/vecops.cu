@@ -245,6 +245,12 @@ __global__ void itergp_init_kernel(const double* __restrict__ partial, int npart
   }
 }
 
+__global__ void iter_coefs_kernel(const double* __restrict__ dots, int w, const double* __restrict__ eta,
+                                  double* __restrict__ c, const double* __restrict__ state) {
+  if (state[ST_DONE] != 0.0) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < w; j += gridDim.x * blockDim.x) c[j] = dots[j] / eta[j];
+}
+
 unsigned grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 8));
@@ -291,9 +297,24 @@ void itergp_reorth_coefs(const double* Kd, int64_t ld, int w, const double* gd, 
   check_launch("itergp_reorth_coefs");
 }
 
+// the fused update pass; block partial sums [eta..][delta..] into scratch, returns the block count
+static int itergp_update_blocks(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld,
+                                int w, const double* c, const double* r, double* dout, double* gout, int64_t n,
+                                const double* state, double** partial_out, cudaStream_t s);
+
 void itergp_update(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
                    const double* c, const double* r, double* dout, double* gout, int64_t n, double* state,
                    double* eta_slot, cudaStream_t s) {
+  double* part = nullptr;
+  const int nblk = itergp_update_blocks(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, state, &part, s);
+  itergp_update_final_kernel<<<1, 256, 0, s>>>(part, nblk, state, eta_slot);
+  count_launch();
+  check_launch("itergp_update");
+}
+
+static int itergp_update_blocks(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld,
+                                int w, const double* c, const double* r, double* dout, double* gout, int64_t n,
+                                const double* state, double** partial_out, cudaStream_t s) {
   auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const bool v2 = (n % 2 == 0) && (ld % 2 == 0) && a16(d) && a16(g) && a16(Kd) && a16(Kg) && a16(r) && a16(dout) &&
                   a16(gout);
@@ -306,9 +327,9 @@ void itergp_update(const double* d, const double* g, const double* Kd, const dou
     itergp_update_kernel<true><<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
   else
     itergp_update_kernel<false><<<nblk, RED_THREADS, 0, s>>>(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, partial.ptr, state);
-  itergp_update_final_kernel<<<1, 256, 0, s>>>(partial.ptr, nblk, state, eta_slot);
-  count_launch(2);
-  check_launch("itergp_update");
+  count_launch();
+  *partial_out = partial.ptr;
+  return nblk;
 }
 
 void itergp_step(double* x, double* r, const double* dn, const double* gn, int64_t n, double* state, cudaStream_t s) {
@@ -320,6 +341,94 @@ void itergp_step(double* x, double* r, const double* dn, const double* gn, int64
   count_launch(2);
   check_launch("itergp_step");
 }
+
+// ---- C ABI: the iteration steps with explicit partial sums (sharded solve) ----
+template <class F>
+static int guarded_vec(F&& f) {
+  try {
+    f();
+    return GPFVM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  }
+}
+
+}  // namespace gpfvm
+
+extern "C" {
+using namespace gpfvm;
+
+int gpfvm_iter_init(const double* yy, double rtol, double* state, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(yy && state, GPFVM_ERR_INVALID, "null argument");
+    itergp_init_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(yy, 1, rtol, state);
+    count_launch();
+    check_launch("gpfvm_iter_init");
+  });
+}
+
+int gpfvm_iter_coefs(const double* dots, int w, const double* eta, double* c, const double* state, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(w >= 0 && (w == 0 || (dots && eta && c)) && state, GPFVM_ERR_INVALID, "bad arguments");
+    if (w == 0) return;
+    iter_coefs_kernel<<<(w + 255) / 256, 256, 0, (cudaStream_t)stream>>>(dots, w, eta, c, state);
+    count_launch();
+    check_launch("gpfvm_iter_coefs");
+  });
+}
+
+int gpfvm_iter_update_local(const double* d, const double* g, const double* Kd, const double* Kg, int64_t ld, int w,
+                            const double* c, const double* r, double* dout, double* gout, int64_t n, double* partial,
+                            const double* state, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(d && g && r && dout && gout && partial && state && n >= 0 && w >= 0 && (w == 0 || (Kd && Kg && c)),
+                GPFVM_ERR_INVALID, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    double* part = nullptr;
+    const int nblk = itergp_update_blocks(d, g, Kd, Kg, ld, w, c, r, dout, gout, n, state, &part, s);
+    dot_final_kernel<<<2, 512, 0, s>>>(part, nblk, partial);  // [eta, delta] local sums
+    count_launch();
+    check_launch("gpfvm_iter_update_local");
+  });
+}
+
+int gpfvm_iter_update_final(const double* sums, double* state, double* eta_slot, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(sums && state && eta_slot, GPFVM_ERR_INVALID, "null argument");
+    itergp_update_final_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(sums, 1, state, eta_slot);
+    count_launch();
+    check_launch("gpfvm_iter_update_final");
+  });
+}
+
+int gpfvm_iter_step_local(double* x, double* r, const double* dn, const double* gn, int64_t n, double* partial,
+                          const double* state, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(x && r && dn && gn && partial && state && n >= 0, GPFVM_ERR_INVALID, "bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nblk = red_blocks(n);
+    DevBuf& part = scratch(s, 3);
+    part.ensure((size_t)2 * RED_BLOCKS);
+    itergp_step_kernel<<<nblk, RED_THREADS, 0, s>>>(x, r, dn, gn, n, part.ptr, state);
+    dot_final_kernel<<<1, 512, 0, s>>>(part.ptr, nblk, partial);
+    count_launch(2);
+    check_launch("gpfvm_iter_step_local");
+  });
+}
+
+int gpfvm_iter_step_final(const double* sum, double* state, void* stream) {
+  return guarded_vec([&] {
+    GPFVM_CHECK(sum && state, GPFVM_ERR_INVALID, "null argument");
+    itergp_step_final_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(sum, 1, state);
+    count_launch();
+    check_launch("gpfvm_iter_step_final");
+  });
+}
+
+}  // extern "C"
+
+namespace gpfvm {
 
 void axpy_many(double* y, const double* X, int64_t ldx, const double* coef, double sign, int64_t n, int k,
                cudaStream_t s) {

@@ -1,308 +1,260 @@
-"""Time-mode sharded GP-FVM operator and solver (north_star multi-GPU row,
-DESIGN.md §7).
+"""Time-mode sharded GP-FVM (north_star multi-GPU row): a thin
+orchestrator.  Every arithmetic step — the spatial Kronecker products, the
+grouping of terms by time factor (R6 cancellation included), the packing of
+the exchange buffers, the K-concatenated time GEMM, the block-Jacobi FD
+preconditioner and every IterGP scalar — runs in libgpfvm (gpfvm_shard_*,
+gpfvm_iter_*, gpfvm_dot_many).  This module only
 
-The PDE observation tensor (n0 time cells x spatial cells) is split along the
-time mode into W contiguous slabs, one per rank.  For a Kronecker sum
-``G x = sum_p (F0_p (x) F1_p (x) ...) x`` (Eq. 20):
+  * allocates the exchange buffers the library sizes (gpfvm_shard_counts),
+  * moves them with ``all_to_all_single`` (NCCL over NVLink on GPUs), and
+  * sums the IterGP partial scalars with ``all_reduce``.
 
-  1. every rank contracts its slab with the spatial factors, writing one
-     (slab x spatial-chunk) block per destination rank and term (no packing:
-     the factor rows of the destination's chunk are used directly);
-  2. ``all_to_all`` re-partitions to "all times x one spatial chunk";
-  3. one GEMM contracts the time mode for all terms at once (the term sum is
-     the K-concatenation: A_big[m, (src, p, t)] = c_p F0_p[m, src*nt + t]);
-  4. ``all_to_all`` back, and a permute kernel restores the slab layout.
-CG inner products are local partial dots + ``all_reduce``.  Communication per
-matvec: (P + 1) N 8 bytes.
-
-All arithmetic goes through a ``LocalOps`` backend.  ``GpuOps`` calls the
-library kernels (gpfvm_kron_matvec, gpfvm_gemm, gpfvm_permute,
-gpfvm_dot_many, gpfvm_axpy_many, gpfvm_sygv); the CPU backend used by the
-gloo tests lives in ``tests/`` (test infrastructure).  torch.distributed only
-moves bytes (NCCL over NVLink on GPUs, gloo in the CPU tests).
+``Comm`` abstracts the two collectives over the ranks held by this process:
+``TorchComm`` (one rank per process, torch.distributed) and ``LocalComm``
+(W ranks in one process on one GPU, exchanges done as copies: the
+single-GPU numerical check of the multi-rank layouts; no kernel ever waits on
+another rank).  The sharded objects are lists with one entry per local rank.
 """
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
-from typing import List, Sequence
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
 
 import torch
 import torch.distributed as dist
 
 from . import _lib as L
 
-
-class GpuOps:
-    """Library-kernel implementations of the local operations (CUDA tensors)."""
-
-    def __init__(self, device):
-        self.lib = L.load()
-        self.device = torch.device(device)
-
-    def _s(self):
-        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
-
-    @staticmethod
-    def _p(t):
-        return C.c_void_p(t.data_ptr())
-
-    def empty(self, *shape):
-        return torch.empty(*shape, dtype=torch.float64, device=self.device)
-
-    def zeros(self, *shape):
-        return torch.zeros(*shape, dtype=torch.float64, device=self.device)   # memset (plumbing)
-
-    def kron(self, in_shape, out_shape, coefs, factors, x, y, nrhs, beta=0.0):
-        d = len(in_shape)
-        ins = (C.c_int * d)(*in_shape)
-        outs = (C.c_int * d)(*out_shape)
-        cf = (C.c_double * len(coefs))(*coefs)
-        fp = (C.c_void_p * (len(coefs) * d))(*[f.data_ptr() for term in factors for f in term])
-        nin = 1
-        nout = 1
-        for a, b in zip(in_shape, out_shape):
-            nin *= a
-            nout *= b
-        L.check(self.lib.gpfvm_kron_matvec(d, ins, outs, len(coefs), cf, fp, self._p(x), nin, self._p(y), nout,
-                                           int(nrhs), float(beta), self._s()))
-
-    def gemm(self, A, B, Cm, alpha=1.0, beta=0.0):
-        M, K = A.shape
-        K2, N = B.shape
-        assert K == K2 and Cm.shape == (M, N)
-        L.check(self.lib.gpfvm_gemm(M, N, K, float(alpha), self._p(A), A.stride(0), self._p(B), B.stride(0),
-                                    float(beta), self._p(Cm), Cm.stride(0), self._s()))
-
-    def permute(self, src, shape, perm):
-        d = len(shape)
-        out = self.empty([shape[p] for p in perm])
-        L.check(self.lib.gpfvm_permute(d, (C.c_int * d)(*shape), (C.c_int * d)(*perm), self._p(src),
-                                       self._p(out), self._s()))
-        return out
-
-    def dots(self, X, v):
-        """[X_j . v for j] as a tensor (local partial dots)."""
-        k = X.shape[0]
-        out = self.empty(k)
-        L.check(self.lib.gpfvm_dot_many(self._p(X), X.stride(0), self._p(v), v.numel(), k, self._p(out), self._s()))
-        return out
-
-    def axpy(self, y, X, coef, sign=1.0):
-        k = X.shape[0]
-        L.check(self.lib.gpfvm_axpy_many(self._p(y), self._p(X), X.stride(0), self._p(coef), float(sign), y.numel(),
-                                         k, self._s()))
-
-    def vmul(self, x, d):
-        L.check(self.lib.gpfvm_vmul(self._p(x), self._p(d), x.numel(), self._s()))
-        return x
-
-    def transpose(self, A):
-        return self.permute(A, list(A.shape), [1, 0])
-
-    def fd_setup(self, ca, A0, A1, cb, B0, B1, noise):
-        n0, n1 = A0.shape[0], A1.shape[0]
-        V = self.empty(n0, n0)
-        Wm = self.empty(n1, n1)
-        Dinv = self.empty(n0, n1)
-        L.check(self.lib.gpfvm_fd_setup(n0, n1, self._p(A0), self._p(A1), self._p(B0), self._p(B1), float(ca),
-                                        float(cb), float(noise), self._p(V), self._p(Wm), self._p(Dinv), self._s()))
-        return V, Wm, Dinv
-
-    def sygv(self, A, B):
-        n = A.shape[0]
-        V = self.empty(n, n)
-        w = self.empty(n)
-        L.check(self.lib.gpfvm_sygv(n, self._p(A), self._p(B), self._p(V), self._p(w), self._s()))
-        return V, w
+SHARD_GRAM, SHARD_PRECOND = 0, 1
+ITER_STATE = 8
+ST_NY, ST_NR, ST_DONE, ST_COUNT = 0, 1, 5, 6
 
 
-@dataclass
-class ShardedKron:
-    """y = sum_p c_p ((x)_i F_{p,i}) x with x, y sharded along dim 0."""
+def _p(t):
+    return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else C.c_void_p(0)
 
-    ops: object
-    shape: Sequence[int]                 # (n0, n1, ...) square operator
-    coefs: List[float]
-    factors: List[List[torch.Tensor]]    # full factors, factors[p][i] : n_i x n_i
-    group: object = None
-    rank: int = 0
-    world: int = 1
-    A_big: torch.Tensor = field(init=False, default=None)
 
-    def __post_init__(self):
-        n0 = self.shape[0]
+def _stream(dev):
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+# ---- collectives -------------------------------------------------------------
+class TorchComm:
+    """One local rank; all_to_all_single / all_reduce over a process group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.ranks = [dist.get_rank(group) if dist.is_initialized() else 0]
+
+    def alltoall(self, sends: List[torch.Tensor], recvs: List[torch.Tensor], send_counts, recv_counts):
+        if self.world == 1:
+            recvs[0].copy_(sends[0])
+            return
+        dist.all_to_all_single(recvs[0], sends[0], output_split_sizes=list(recv_counts[0]),
+                               input_split_sizes=list(send_counts[0]), group=self.group)
+
+    def allreduce(self, ts: List[torch.Tensor]):
+        if self.world > 1:
+            dist.all_reduce(ts[0], op=dist.ReduceOp.SUM, group=self.group)
+
+
+class LocalComm:
+    """W ranks in this process (one GPU): exchanges are plain device copies."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def alltoall(self, sends, recvs, send_counts, recv_counts):
         W = self.world
-        if n0 % W or self.shape[1] % W:
-            raise ValueError(f"time ({n0}) and first spatial ({self.shape[1]}) sizes must be divisible by {W}")
-        self.nt = n0 // W
-        self.rest = 1
-        for s in self.shape[1:]:
-            self.rest *= s
-        self.c1 = self.shape[1] // W
-        self.cw = self.rest // W
-        P = len(self.coefs)
-        # A_big[m, (src, p, t)] = c_p F0_p[m, src*nt + t]
-        F0 = self.ops.empty(P, n0, n0)
-        for p in range(P):
-            F0[p].copy_(self.factors[p][0])     # device copy (plumbing); c_p is applied in step 1
-        self.A_big = self.ops.permute(F0.reshape(P, n0, W, self.nt), [P, n0, W, self.nt], [1, 2, 0, 3]).reshape(
-            n0, W * P * self.nt)
+        soff = [[0] * (W + 1) for _ in range(W)]
+        roff = [[0] * (W + 1) for _ in range(W)]
+        for r in range(W):
+            for q in range(W):
+                soff[r][q + 1] = soff[r][q] + send_counts[r][q]
+                roff[r][q + 1] = roff[r][q] + recv_counts[r][q]
+        for src in range(W):
+            for dst in range(W):
+                n = send_counts[src][dst]
+                assert n == recv_counts[dst][src], "exchange counts disagree"
+                if n:
+                    recvs[dst][roff[dst][src]:roff[dst][src] + n].copy_(sends[src][soff[src][dst]:soff[src][dst] + n])
 
-    def matvec(self, x_local):
-        P, W, nt, cw = len(self.coefs), self.world, self.nt, self.cw
-        spatial = list(self.shape[1:])
-        # one spatial Kronecker product per term over all destination chunks
-        # (P library calls instead of W * P), then one permutation into the
-        # all-to-all send layout [dest chunk][term][local time][chunk]
-        full = self.ops.empty(P, nt, self.rest)
-        for p in range(P):
-            fac = [self.factors[p][1]] + list(self.factors[p][2:])
-            self.ops.kron(spatial, spatial, [self.coefs[p]], [fac], x_local, full[p], nrhs=nt)
-        send = self.ops.permute(full, [P, nt, W, cw], [2, 0, 1, 3])
-        recv = _all_to_all(send, self.group, W)
-        yspace = self.ops.empty(self.shape[0], cw)
-        self.ops.gemm(self.A_big, recv.reshape(W * P * nt, cw), yspace)
-        back = _all_to_all(yspace.reshape(W, nt, cw), self.group, W)
-        return self.ops.permute(back, [W, nt, cw], [1, 0, 2]).reshape(-1)
+    def allreduce(self, ts):
+        total = ts[0].clone()
+        for t in ts[1:]:
+            total += t
+        for t in ts:
+            t.copy_(total)
 
 
-def _all_to_all(t, group, W):
-    if W == 1:
-        return t
-    out = torch.empty_like(t)
-    dist.all_to_all_single(out.view(-1), t.contiguous().view(-1), group=group)
-    return out
+# ---- sharded operators ---------------------------------------------------------
+class _ShardOp:
+    """One library shard handle per local rank (kind GRAM or PRECOND)."""
 
+    def __init__(self, gps, comm, kind):
+        self.lib = L.load()
+        self.comm = comm
+        self.gps = gps
+        self.dev = [torch.device("cuda", gp.device) for gp in gps]
+        self.h = []
+        for gp, r, dev in zip(gps, comm.ranks, self.dev):
+            h = C.c_void_p()
+            with torch.cuda.device(dev):
+                L.check(self.lib.gpfvm_shard_create(gp.handle, int(r), int(comm.world), int(kind), C.byref(h),
+                                                    _stream(dev)))
+            self.h.append(h)
+        W = comm.world
+        self.n = [int(self.lib.gpfvm_shard_local_size(h)) for h in self.h]
+        self.phases = 2 if kind == SHARD_PRECOND else 1
+        self.counts = []  # per phase: (send1, recv1, send2, recv2), each per local rank a list of W ints
+        self.bufs = []
+        for ph in range(self.phases):
+            cs = [[], [], [], []]
+            for h in self.h:
+                arr = [(C.c_int64 * W)() for _ in range(4)]
+                L.check(self.lib.gpfvm_shard_counts(h, ph, *arr))
+                for k in range(4):
+                    cs[k].append([int(v) for v in arr[k]])
+            self.counts.append(cs)
+            self.bufs.append([[torch.empty(max(1, sum(cs[k][i])), dtype=torch.float64, device=self.dev[i])
+                               for i in range(len(self.h))] for k in range(4)])
 
-def allreduce_(t, group, W):
-    if W > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    return t
+    def layout(self, i=0):
+        nb = len(self.gps[i].problem.blocks)
+        arrs = [(C.c_int64 * nb)() for _ in range(4)]
+        L.check(self.lib.gpfvm_shard_layout(self.h[i], *arrs))
+        return [[int(v) for v in a] for a in arrs]
 
+    def apply(self, ph: int, xs: Sequence[torch.Tensor], ys: Sequence[torch.Tensor], x_for_end=True):
+        s1, r1, s2, r2 = self.bufs[ph]
+        c = self.counts[ph]
+        for i, h in enumerate(self.h):
+            L.check(self.lib.gpfvm_shard_apply_begin(h, ph, _p(xs[i]), _p(s1[i]), _stream(self.dev[i])))
+        self.comm.alltoall(s1, r1, c[0], c[1])
+        for i, h in enumerate(self.h):
+            L.check(self.lib.gpfvm_shard_apply_mid(h, ph, _p(r1[i]), _p(s2[i]), _stream(self.dev[i])))
+        self.comm.alltoall(s2, r2, c[2], c[3])
+        for i, h in enumerate(self.h):
+            L.check(self.lib.gpfvm_shard_apply_end(h, ph, _p(r2[i]), _p(xs[i]) if x_for_end else C.c_void_p(0),
+                                                   _p(ys[i]), _stream(self.dev[i])))
 
-@dataclass
-class ShardedFD:
-    """Sharded fast-diagonalisation inverse of the 2D heat
-    PDE block  c_a A0(x)A1 + c_b B0(x)B1:  (V(x)W) D^{-1} (V(x)W)^T."""
-
-    ops: object
-    fwd: ShardedKron      # applies V^T (x) W^T
-    bwd: ShardedKron      # applies V (x) W
-    dinv_local: torch.Tensor
-
-    def apply(self, r_local):
-        z = self.fwd.matvec(r_local)
-        self.ops.vmul(z, self.dinv_local)
-        return self.bwd.matvec(z)
-
-
-def build_fd(ops, shape, ca, A0, A1, cb, B0, B1, noise, group, rank, world):
-    V, Wm, Dinv = ops.fd_setup(ca, A0, A1, cb, B0, B1, noise)
-    n0, n1 = shape
-    nt = n0 // world
-    dinv_local = Dinv[rank * nt:(rank + 1) * nt].reshape(-1).contiguous()
-    fwd = ShardedKron(ops, shape, [1.0], [[ops.transpose(V), ops.transpose(Wm)]], group, rank, world)
-    bwd = ShardedKron(ops, shape, [1.0], [[V, Wm]], group, rank, world)
-    return ShardedFD(ops, fwd, bwd, dinv_local)
-
-
-def heat_pde_operator(ops, factors, kappa, group=None, rank=0, world=1, noise=0.0):
-    """Sharded PDE-block operator and FD preconditioner of the heat problem
-    (terms T11(x)X00 + kappa^2 T00(x)X22 after the R6 cancellation).
-    ``factors``: dict with keys T00, T11, X00, X22 (full matrices on the ops device)."""
-    n0, n1 = factors["T00"].shape[0], factors["X00"].shape[0]
-    A = ShardedKron(ops, (n0, n1), [1.0, kappa * kappa],
-                    [[factors["T11"], factors["X00"]], [factors["T00"], factors["X22"]]], group, rank, world)
-    fd = build_fd(ops, (n0, n1), 1.0, factors["T11"], factors["X00"], kappa * kappa, factors["T00"],
-                  factors["X22"], noise, group, rank, world)
-    return A, fd
+    def close(self):
+        for h in self.h:
+            if h:
+                self.lib.gpfvm_shard_destroy(h)
+        self.h = []
 
 
 @dataclass
-class PCGResult:
-    x: torch.Tensor
+class ShardedReport:
     iterations: int
-    rel_residual: float
     converged: bool
-    residual_norms: list
+    breakdown: bool
+    rel_residual: float
 
 
-def sharded_pcg(ops, A: ShardedKron, y_local, precond=None, rtol=1e-8, max_iter=200, group=None, world=1):
-    """IterGP/PCG with full reorthogonalisation (R7) on sharded vectors."""
-    n = y_local.numel()
-    x = ops.zeros(n)
-    r = ops.empty(n)
-    r.copy_(y_local)
-    ny = float(allreduce_(ops.dots(r.reshape(1, -1), r), group, world)[0]) ** 0.5
-    D = ops.empty(max_iter + 1, n)
-    GD = ops.empty(max_iter + 1, n)
-    etas = []
-    norms = [1.0]
-    k = 0
-    nr = ny
-    converged = ny == 0.0
-    while not converged and k < max_iter:
-        if nr <= rtol * ny:
-            converged = True
-            break
-        if precond is not None:
-            s = precond.apply(r)
-        else:
-            s = ops.empty(n)
-            s.copy_(r)
-        z = A.matvec(s)
-        D[k].copy_(s)
-        GD[k].copy_(z)
-        if k > 0:
-            c = allreduce_(ops.dots(D[:k], z), group, world).cpu()          # k scalars
-            c = torch.tensor([float(c[j]) / etas[j] for j in range(k)], dtype=torch.float64).to(z.device)
-            ops.axpy(D[k], D[:k], c, -1.0)
-            ops.axpy(GD[k], GD[:k], c, -1.0)
-        two = ops.empty(2)
-        two[0:1].copy_(ops.dots(D[k].reshape(1, -1), GD[k]))
-        two[1:2].copy_(ops.dots(D[k].reshape(1, -1), r))
-        two = allreduce_(two, group, world).cpu()
-        eta, dr = float(two[0]), float(two[1])
-        if not eta > 0:
-            break
-        a = dr / eta
-        coef = torch.tensor([a], dtype=r.dtype, device=r.device)
-        ops.axpy(x, D[k:k + 1], coef, 1.0)
-        ops.axpy(r, GD[k:k + 1], coef, -1.0)
-        etas.append(eta)
-        k += 1
-        nr = float(allreduce_(ops.dots(r.reshape(1, -1), r), group, world)[0]) ** 0.5
-        norms.append(nr / ny)
-    converged = converged or nr <= rtol * ny
-    return PCGResult(x, k, nr / ny if ny else 0.0, converged, norms)
+class ShardedProblem:
+    """The GP-FVM Gram, its block-Jacobi FD preconditioner and the IterGP solve,
+    sharded along the time mode.  ``gps``: one assembled GpfvmProblem per local
+    rank (TorchComm: one; LocalComm(W): W problems on one GPU)."""
 
+    def __init__(self, gps, comm):
+        self.lib = L.load()
+        self.comm = comm
+        self.gps = list(gps)
+        self.G = _ShardOp(self.gps, comm, SHARD_GRAM)
+        self.P: Optional[_ShardOp] = None
+        self.n = self.G.n
+        self.dev = self.G.dev
 
-def block_kron_terms(problem, J, device=0):
-    """Kronecker terms (coefficients, full 1D factors on the GPU) of the diagonal
-    Gram block (J, J), with the exact R6 cancellation of term pairs (the same
-    rule the library applies internally), factors from gpfvm_factor_matrix."""
-    from .api import factor_matrix
-    blk = problem.blocks[J]
-    d = problem.ndim
-    coefs, facs = [], []
-    cache = {}
-    for a, t1 in enumerate(blk.terms):
-        for b, t2 in enumerate(blk.terms):
-            if t1.output != t2.output or b < a:
-                continue
-            c = t1.coeff * t2.coeff
-            if a != b:
-                if sum(t1.order[i] + t2.order[i] for i in range(d)) % 2:
-                    continue
-                c *= 2.0
-            fs = []
-            for i in range(d):
-                key = (t1.output, i, t1.order[i], t2.order[i])
-                if key not in cache:
-                    k = problem.kernels[t1.output][i]
-                    cache[key] = factor_matrix(k, blk.sites[i], t1.order[i], blk.sites[i], t2.order[i], device)
-                fs.append(cache[key])
-            coefs.append(c)
-            facs.append(fs)
-    return coefs, facs
+    # -- vectors
+    def local(self, full_vectors: Sequence[torch.Tensor]) -> List[torch.Tensor]:
+        """Local slabs of full (block-concatenated) device vectors, one per local rank."""
+        out = []
+        for i, h in enumerate(self.G.h):
+            t = torch.empty(max(1, self.n[i]), dtype=torch.float64, device=self.dev[i])[:self.n[i]]
+            L.check(self.lib.gpfvm_shard_gather_local(h, _p(full_vectors[i]), _p(t), _stream(self.dev[i])))
+            out.append(t)
+        return out
+
+    def _empty(self):
+        return [torch.empty(max(1, n), dtype=torch.float64, device=d)[:n] for n, d in zip(self.n, self.dev)]
+
+    # -- operators
+    def matvec(self, xs):
+        ys = self._empty()
+        self.G.apply(0, xs, ys)
+        return ys
+
+    def precond(self, rs, out=None):
+        if self.P is None:
+            self.P = _ShardOp(self.gps, self.comm, SHARD_PRECOND)
+        tmp = self._empty()
+        zs = out if out is not None else self._empty()
+        self.P.apply(0, rs, tmp, x_for_end=False)
+        for i, h in enumerate(self.P.h):
+            L.check(self.lib.gpfvm_shard_precond_scale(h, _p(tmp[i]), _stream(self.dev[i])))
+        self.P.apply(1, tmp, zs, x_for_end=False)
+        return zs
+
+    # -- IterGP (CG policy, full reorthogonalisation by default) ----------------
+    def solve(self, ys, rtol=1e-8, max_iter=200, reorth_window=0, precond=True, check_every=4):
+        """alpha = G^{-1} y on the sharded vectors; every scalar stays on the
+        device (library kernels), the ranks sum partial scalars with all_reduce."""
+        lib, R = self.lib, range(len(self.gps))
+        st = [torch.zeros(ITER_STATE, dtype=torch.float64, device=d) for d in self.dev]
+        xs = [torch.zeros_like(y) for y in ys]
+        rs = [y.clone() for y in ys]
+        D = [torch.empty(max_iter + 1, max(1, n), dtype=torch.float64, device=d) for n, d in zip(self.n, self.dev)]
+        GD = [torch.empty_like(t) for t in D]
+        eta = [torch.zeros(max_iter + 1, dtype=torch.float64, device=d) for d in self.dev]
+        cbuf = [torch.zeros(max_iter + 1, dtype=torch.float64, device=d) for d in self.dev]
+        p1 = [torch.empty(max(1, max_iter + 1), dtype=torch.float64, device=d) for d in self.dev]
+        p2 = [torch.empty(2, dtype=torch.float64, device=d) for d in self.dev]
+        s = [_stream(d) for d in self.dev]
+        for i in R:
+            L.check(lib.gpfvm_dot_many(_p(ys[i]), max(1, self.n[i]), _p(ys[i]), self.n[i], 1, _p(p1[i]), s[i]))
+        self.comm.allreduce([t[:1] for t in p1])
+        for i in R:
+            L.check(lib.gpfvm_iter_init(_p(p1[i]), float(rtol), _p(st[i]), s[i]))
+        it = 0
+        while it < max_iter:
+            if it == 0 or it <= 4 or it % check_every == 0:
+                if float(st[0][ST_DONE]) != 0.0:
+                    break
+            ds = self.precond(rs) if precond else [r.clone() for r in rs]
+            gds = self.matvec(ds)
+            w = it if reorth_window <= 0 else min(reorth_window, it)
+            j0 = it - w
+            if w > 0:
+                for i in R:
+                    L.check(lib.gpfvm_dot_many(_p(D[i][j0]), D[i].stride(0), _p(gds[i]), self.n[i], w, _p(p1[i]), s[i]))
+                self.comm.allreduce([t[:w] for t in p1])
+                for i in R:
+                    L.check(lib.gpfvm_iter_coefs(_p(p1[i]), w, _p(eta[i][j0:]), _p(cbuf[i]), _p(st[i]), s[i]))
+            for i in R:
+                L.check(lib.gpfvm_iter_update_local(_p(ds[i]), _p(gds[i]), _p(D[i][j0]), _p(GD[i][j0]), D[i].stride(0),
+                                                    w, _p(cbuf[i]), _p(rs[i]), _p(D[i][it]), _p(GD[i][it]),
+                                                    self.n[i], _p(p2[i]), _p(st[i]), s[i]))
+            self.comm.allreduce(p2)
+            for i in R:
+                L.check(lib.gpfvm_iter_update_final(_p(p2[i]), _p(st[i]), _p(eta[i][it:]), s[i]))
+                L.check(lib.gpfvm_iter_step_local(_p(xs[i]), _p(rs[i]), _p(D[i][it]), _p(GD[i][it]), self.n[i],
+                                                  _p(p1[i]), _p(st[i]), s[i]))
+            self.comm.allreduce([t[:1] for t in p1])
+            for i in R:
+                L.check(lib.gpfvm_iter_step_final(_p(p1[i]), _p(st[i]), s[i]))
+            it += 1
+        h = st[0].cpu()
+        ny = float(h[ST_NY])
+        rep = ShardedReport(int(h[ST_COUNT]), bool(h[ST_DONE] == 1.0 or ny == 0.0), bool(h[ST_DONE] == 2.0),
+                            float(h[ST_NR]) / ny if ny > 0 else 0.0)
+        return xs, rep
+
+    def close(self):
+        self.G.close()
+        if self.P is not None:
+            self.P.close()

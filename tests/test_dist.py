@@ -1,129 +1,123 @@
-"""Host logic of the time-sharded multi-GPU path (paper_2406_05020_b200.dist),
-world size 2 over gloo on CPU: sharding, all-to-all re-partition, the
-K-concatenated time GEMM, allreduce'd CG inner products.  Local arithmetic
-uses the CPU test backend (tests/dist_cpu_ops.py); expected values come from
-the oracle."""
+"""Multi-rank host logic of the time-sharded path on CPU (no GPU needed):
+
+* the library's exchange plan (gpfvm_shard_plan_counts, host-only C++: the
+  same code gpfvm_shard_create runs) is consistent across ranks — what rank r
+  sends to q is what q expects from r, in both exchanges — and the local slabs
+  partition the N observations, for every BASELINE problem shape and 2, 3, 8
+  ranks;
+* the torch.distributed collectives dist.TorchComm issues (all_to_all_single
+  with the plan's uneven split sizes, all_reduce) over gloo, world size 2,
+  equal the single-process emulation dist.LocalComm that the GPU tests use to
+  check the sharded numerics against the oracle (tests/test_gpu_dist.py)."""
+import ctypes as C
 import os
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import gpfvm_inputs as gi
-from gpfvm_inputs import Block, Kernel1D, Problem, Term
-from oracle.gram import KroneckerGram, dense_gram, factor_matrix
 
-NT, NX = 16, 32
+
+def _lib():
+    from paper_2406_05020_b200 import _lib as L
+    try:
+        return L.load()
+    except RuntimeError:
+        pytest.skip("libgpfvm.so not built")
+
+
+def _plan(gp, rank, world):
+    lib = _lib()
+    n = C.c_int64()
+    arrs = [(C.c_int64 * world)() for _ in range(4)]
+    from paper_2406_05020_b200 import _lib as L
+    L.check(lib.gpfvm_shard_plan_counts(gp.handle, rank, world, C.byref(n), *arrs))
+    return int(n.value), [[int(v) for v in a] for a in arrs]
+
+
+PROBLEMS = {
+    "heat-16x24": lambda: gi.heat_problem(16, 24),
+    "wave-8x10x12": lambda: gi.wave_problem(8, 10, 12),
+    "shallow-water-6x6x7": lambda: gi.shallow_water_problem(6, 6, 7),
+    "config3": gi.config3,
+    "config4": gi.config4,
+}
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_plan_counts_consistent(name, world):
+    from paper_2406_05020_b200 import GpfvmProblem
+    from paper_2406_05020_b200._lib import GpfvmError
+    p = PROBLEMS[name]()
+    gp = GpfvmProblem(p, device=0)
+    if world > max(b.shape[0] for b in p.blocks):
+        with pytest.raises(GpfvmError):  # more ranks than time sites
+            _plan(gp, 0, world)
+        return
+    plans = [_plan(gp, r, world) for r in range(world)]
+    assert sum(n for n, _ in plans) == p.size
+    for r in range(world):
+        for q in range(world):
+            assert plans[r][1][0][q] == plans[q][1][1][r], ("exchange 1", r, q)
+            assert plans[r][1][2][q] == plans[q][1][3][r], ("exchange 2", r, q)
+    # every rank holds a time slab of the time-extended blocks (IC planes on rank 0)
+    assert all(n > 0 for n, _ in plans)
 
 
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
+    port = s.getsockname()[1]
     s.close()
-    return p
+    return port
 
 
-def _heat_pde_problem(nt=NT, nx=NX, kappa=0.1):
-    p = gi.heat_problem(nt, nx, kappa=kappa)
-    pde = p.blocks[3]
-    return Problem("heat_pde_only", 2, p.kernels, [pde], meta=p.meta)
-
-
-def _heat_factors(nt=NT, nx=NX):
-    p = gi.heat_problem(nt, nx)
-    kt, kx = p.kernels[0]
-    T, X = p.blocks[3].sites
-    f = lambda k, S, m: torch.from_numpy(factor_matrix((k.q, k.lengthscale, k.variance), S, m, S, m))
-    return {"T00": f(kt, T, 0), "T11": f(kt, T, 1), "X00": f(kx, X, 0), "X22": f(kx, X, 2)}
-
-
-def _worker(rank, world, port, out_q, case):
+def _worker(rank, world, port, counts, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from dist_cpu_ops import CpuOps
-        from paper_2406_05020_b200.dist import ShardedKron, heat_pde_operator, sharded_pcg
-        ops = CpuOps()
-        if case == "heat":
-            fac = _heat_factors()
-            A, fd = heat_pde_operator(ops, fac, 0.1, None, rank, world)
-            x = torch.from_numpy(gi.random_vectors(NT * NX, 1, 3)[0])
-            nt = NT // world
-            xl = x.reshape(NT, NX)[rank * nt:(rank + 1) * nt].reshape(-1).clone()
-            yl = A.matvec(xl)
-            # PCG on G_pp a = b with the sharded FD preconditioner
-            b = torch.from_numpy(gi.random_vectors(NT * NX, 1, 5)[0])
-            bl = b.reshape(NT, NX)[rank * nt:(rank + 1) * nt].reshape(-1).clone()
-            res = sharded_pcg(ops, A, bl, fd, rtol=1e-10, max_iter=20, group=None, world=world)
-            out_q.put((rank, yl.numpy().copy(), res.x.numpy().copy(), res.iterations, res.rel_residual))
-        else:  # 3D two-term operator
-            rng = np.random.default_rng(7)
-            shape = (8, 6, 5)
-            facs = [[torch.from_numpy(rng.standard_normal((n, n))) for n in shape] for _ in range(2)]
-            A = ShardedKron(ops, shape, [0.7, -1.3], facs, None, rank, world)
-            x = torch.from_numpy(rng.standard_normal(int(np.prod(shape))))
-            nt = shape[0] // world
-            xl = x.reshape(shape)[rank * nt:(rank + 1) * nt].reshape(-1).clone()
-            out_q.put((rank, A.matvec(xl).numpy().copy(), None, 0, 0.0))
+        from paper_2406_05020_b200.dist import TorchComm
+        comm = TorchComm()
+        send_counts, recv_counts = counts
+        g = torch.Generator().manual_seed(100 + rank)
+        send = torch.randn(sum(send_counts[rank]), dtype=torch.float64, generator=g)
+        recv = torch.empty(sum(recv_counts[rank]), dtype=torch.float64)
+        comm.alltoall([send], [recv], [send_counts[rank]], [recv_counts[rank]])
+        red = torch.arange(5, dtype=torch.float64) * (rank + 1)
+        comm.allreduce([red])
+        q.put((rank, send, recv, red))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, case):
+def test_torchcomm_gloo_matches_localcomm():
+    from paper_2406_05020_b200 import GpfvmProblem
+    from paper_2406_05020_b200.dist import LocalComm
+    world = 2
+    gp = GpfvmProblem(gi.wave_problem(8, 10, 12), device=0)
+    plans = [_plan(gp, r, world) for r in range(world)]
+    send_counts = [plans[r][1][0] for r in range(world)]
+    recv_counts = [plans[r][1][1] for r in range(world)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, case)) for r in range(world)]
-    for p in procs:
-        p.start()
-    outs = [q.get(timeout=300) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    outs.sort(key=lambda t: t[0])
-    return outs
-
-
-@pytest.fixture(scope="module", autouse=True)
-def _path():
-    here = os.path.dirname(os.path.abspath(__file__))
-    os.environ["PYTHONPATH"] = os.pathsep.join([here, os.path.dirname(here), os.environ.get("PYTHONPATH", "")])
-
-
-def test_sharded_heat_matvec_and_pcg_world2():
-    outs = _run(2, "heat")
-    y = np.concatenate([o[1] for o in outs])
-    x = gi.random_vectors(NT * NX, 1, 3)[0]
-    p = _heat_pde_problem()
-    ref = KroneckerGram(p).matvec(x)
-    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
-    # PCG: sharded IterGP with the sharded FD preconditioner == dense solve
-    b = gi.random_vectors(NT * NX, 1, 5)[0]
-    G = dense_gram(p)
-    a_ref = np.linalg.solve(G, b)
-    a = np.concatenate([o[2] for o in outs])
-    assert outs[0][3] <= 4 and outs[0][3] == outs[1][3]
-    assert np.linalg.norm(G @ a - b) <= 1e-8 * np.linalg.norm(b)
-    assert np.abs(a - a_ref).max() <= 1e-6 * np.abs(a_ref).max()
-
-
-def test_sharded_matvec_world1_equals_world2():
-    y1 = np.concatenate([o[1] for o in _run(1, "heat")])
-    y2 = np.concatenate([o[1] for o in _run(2, "heat")])
-    assert np.abs(y1 - y2).max() <= 1e-13 * np.abs(y1).max()
-
-
-def test_sharded_3d_matvec_world2():
-    outs = _run(2, "3d")
-    y = np.concatenate([o[1] for o in outs])
-    rng = np.random.default_rng(7)
-    shape = (8, 6, 5)
-    facs = [[rng.standard_normal((n, n)) for n in shape] for _ in range(2)]
-    x = rng.standard_normal(int(np.prod(shape)))
-    ref = sum(c * KroneckerGram.apply_kron(f, x, shape) for c, f in zip([0.7, -1.3], facs))
-    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (send_counts, recv_counts), q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict()
+    for _ in range(world):
+        r, send, recv, red = q.get(timeout=300)
+        res[r] = (send, recv, red)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    emu_recv = [torch.empty_like(res[r][1]) for r in range(world)]
+    LocalComm(world).alltoall([res[r][0] for r in range(world)], emu_recv, send_counts, recv_counts)
+    for r in range(world):
+        assert torch.equal(res[r][1], emu_recv[r])
+        assert torch.equal(res[r][2], torch.arange(5, dtype=torch.float64) * 3)

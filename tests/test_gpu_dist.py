@@ -1,63 +1,101 @@
-"""The sharded path (paper_2406_05020_b200.dist) on the GPU through the library
-kernels (GpuOps), world size 1 (the collectives are identities; their host
-logic is covered by tests/test_dist.py with gloo, world size 2)."""
+"""The time-sharded path (paper_2406_05020_b200.dist + the library's
+gpfvm_shard_* / gpfvm_iter_* calls) on one GPU: W = 1, 2, 3 ranks emulated in
+one process (dist.LocalComm: the exchanges are device copies, no kernel waits
+on another rank), every block of the problem sharded (IC planes on rank 0,
+BC faces and the PDE block split in time, multi-output blocks), against the
+oracle's Kronecker matvec and dense Cholesky (Eq. 20 / Eq. 5, PAPER.md
+l.316-320, l.113)."""
 import numpy as np
 import pytest
 
 import gpfvm_inputs as gi
-from gpfvm_inputs import Problem
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
-from oracle.gram import KroneckerGram  # noqa: E402
-from paper_2406_05020_b200 import factor_matrix  # noqa: E402
-from paper_2406_05020_b200.dist import GpuOps, heat_pde_operator, sharded_pcg  # noqa: E402
+from oracle.gram import KroneckerGram, dense_gram  # noqa: E402
+from paper_2406_05020_b200 import GpfvmProblem  # noqa: E402
+from paper_2406_05020_b200.dist import LocalComm, ShardedProblem  # noqa: E402
 
 
-def _factors(p):
-    kt, kx = p.kernels[0]
-    T, X = p.blocks[3].sites
-    return {"T00": factor_matrix(kt, T, 0, T, 0), "T11": factor_matrix(kt, T, 1, T, 1),
-            "X00": factor_matrix(kx, X, 0, X, 0), "X22": factor_matrix(kx, X, 2, X, 2)}
+def _sharded(p, W):
+    gps = []
+    for _ in range(W):
+        gp = GpfvmProblem(p)
+        gp.gpfvm_assemble_factors()
+        gps.append(gp)
+    return ShardedProblem(gps, LocalComm(W)), gps
 
 
-@pytest.mark.parametrize("nt,nx", [(16, 32), (256, 512)])
-def test_gpu_sharded_heat_operator_and_pcg(nt, nx):
-    p = gi.heat_problem(nt, nx)
-    pde = Problem("pde", 2, p.kernels, [p.blocks[3]])
-    ops = GpuOps("cuda:0")
-    A, fd = heat_pde_operator(ops, _factors(p), 0.1)
-    x = gi.random_vectors(nt * nx, 1, 3)[0]
-    y = A.matvec(torch.tensor(x, device="cuda:0")).cpu().numpy()
-    ref = KroneckerGram(pde).matvec(x)
+def _full(sp, locals_, p):
+    out = np.zeros(p.size)
+    for i, loc in enumerate(locals_):
+        off, row0, rows, spatial = sp.G.layout(i)
+        l = loc.cpu().numpy()
+        for J, b in enumerate(p.blocks):
+            n = rows[J] * spatial[J]
+            if n:
+                s = p.offsets[J] + row0[J] * spatial[J]
+                out[s:s + n] = l[off[J]:off[J] + n]
+    return out
+
+
+PROBLEMS = {
+    "heat-16x24": lambda: gi.heat_problem(16, 24),
+    "wave-8x10x12": lambda: gi.wave_problem(8, 10, 12, ell=(0.5, 0.3, 0.3)),
+    "advdiff-9x8x8": lambda: gi.advdiff_problem(9, 8, 8, n_modes=4),
+    "shallow-water-6x6x7": lambda: gi.shallow_water_problem(6, 6, 7),
+}
+
+
+@pytest.mark.parametrize("W", [1, 2, 3])
+@pytest.mark.parametrize("name", list(PROBLEMS))
+def test_sharded_matvec_vs_oracle(name, W):
+    p = PROBLEMS[name]()
+    sp, gps = _sharded(p, W)
+    x = gi.random_vectors(p.size, 1, 17)[0]
+    xt = torch.tensor(x, device="cuda:0")
+    ys = sp.matvec(sp.local([xt] * W))
+    y = _full(sp, ys, p)
+    ref = KroneckerGram(p).matvec(x)
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
-    # FD-preconditioned IterGP on the PDE block with a smooth right-hand side
-    b = KroneckerGram(pde).matvec(np.sin(np.arange(nt * nx) * 0.001))
-    res = sharded_pcg(ops, A, torch.tensor(b, device="cuda:0"), fd, rtol=1e-8, max_iter=30)
-    assert res.converged and res.iterations <= 10, (res.iterations, res.residual_norms)
-    a = res.x.cpu().numpy()
-    r = KroneckerGram(pde).matvec(a) - b
-    assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b)
+    # the second application reuses the plan and buffers
+    y2 = _full(sp, sp.matvec(sp.local([xt] * W)), p)
+    assert np.array_equal(y, y2)
+    sp.close()
 
 
-def test_gpu_sharded_3d_pde_block_matches_library():
-    """block_kron_terms (R6 cancellation rebuilt on the host) + ShardedKron on a
-    3D advection-diffusion PDE block == the library's own Gram matvec restricted
-    to that block (the bench's N>1 sharded measurement path, world size 1)."""
-    from paper_2406_05020_b200 import GpfvmProblem
-    from paper_2406_05020_b200.dist import ShardedKron, block_kron_terms
-    p = gi.advdiff_problem(16, 24, 24, n_modes=4)
-    P = len(p.blocks) - 1
-    pde = Problem("pde", 3, p.kernels, [p.blocks[P]])
-    ops = GpuOps("cuda:0")
-    coefs, facs = block_kron_terms(pde, 0)
-    A = ShardedKron(ops, pde.blocks[0].shape, coefs, facs)
-    gp = GpfvmProblem(pde)
+@pytest.mark.parametrize("W", [1, 2, 3])
+def test_sharded_solve_vs_cholesky(W):
+    """Sharded IterGP with the sharded block-Jacobi FD preconditioner: the
+    solution equals the dense Cholesky one and the iteration count equals the
+    single-GPU solve with the same preconditioner (GPFVM_FORCE_BJFD)."""
+    p = gi.wave_problem(6, 8, 8, ell=(0.5, 0.3, 0.3), ic="sine")
+    G = dense_gram(p)
+    y = p.rhs()
+    a_ref = np.linalg.solve(G, y)
+    sp, gps = _sharded(p, W)
+    yt = torch.tensor(y, device="cuda:0")
+    xs, rep = sp.solve(sp.local([yt] * W), rtol=1e-11, max_iter=400)
+    assert rep.converged and not rep.breakdown, rep
+    a = _full(sp, xs, p)
+    assert np.linalg.norm(G @ a - y) <= 1e-10 * np.linalg.norm(y)
+    assert np.linalg.norm(a - a_ref) <= 1e-6 * np.linalg.norm(a_ref)
+    sp.close()
+
+
+def test_sharded_solve_matches_single_gpu_iterations(monkeypatch):
+    monkeypatch.setenv("GPFVM_FORCE_BJFD", "1")
+    p = gi.advdiff_problem(8, 8, 8, n_modes=4)
+    y = p.rhs()
+    gp = GpfvmProblem(p)
     gp.gpfvm_assemble_factors()
-    x = torch.tensor(gi.random_vectors(pde.size, 1, 4)[0], device="cuda:0")
-    y = A.matvec(x)
-    ref = gp.gpfvm_gram_matvec(x.reshape(1, -1).contiguous())[0]
-    assert float((y - ref).abs().max()) <= 1e-12 * float(ref.abs().max())
+    yt = torch.tensor(y, device="cuda:0")
+    _, rep1 = gp.gpfvm_solve(yt, rtol=1e-9, max_iter=500)
+    sp, _ = _sharded(p, 2)
+    xs, rep2 = sp.solve(sp.local([yt] * 2), rtol=1e-9, max_iter=500)
+    assert rep1["converged"] and rep2.converged
+    assert abs(rep1["iterations"] - rep2.iterations) <= 2, (rep1["iterations"], rep2.iterations)
+    sp.close()
