@@ -592,9 +592,12 @@ void run_gemm(const Gemm& g0, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch1 <= 0 || g.batch2 <= 0 || g.batch3 <= 0) return;
   static const bool trace = getenv("GPFVM_TRACE_GEMM") != nullptr;
   if (trace)
-    fprintf(stderr, "[gemm] M=%d N=%d K=%d nseg=%d batch=%d,%d,%d a(rs=%lld cs=%lld) b(rs=%lld cs=%lld) c(rs=%lld cs=%lld) beta=%g\n",
-            g.M, g.N, g.K, g.nseg, g.batch1, g.batch2, g.batch3, (long long)g.a_rs, (long long)g.a_cs, (long long)g.b_rs,
-            (long long)g.b_cs, (long long)g.c_rs, (long long)g.c_cs, g.beta);
+    fprintf(stderr, "[gemm] M=%d N=%d K=%d nseg=%d batch=%d,%d,%d a(rs=%lld cs=%lld b=%lld,%lld,%lld sg=%lld) "
+            "b(rs=%lld cs=%lld b=%lld,%lld,%lld sg=%lld) c(rs=%lld cs=%lld b=%lld,%lld,%lld) beta=%g\n",
+            g.M, g.N, g.K, g.nseg, g.batch1, g.batch2, g.batch3, (long long)g.a_rs, (long long)g.a_cs, (long long)g.a_b1,
+            (long long)g.a_b2, (long long)g.a_b3, (long long)g.a_sg, (long long)g.b_rs, (long long)g.b_cs,
+            (long long)g.b_b1, (long long)g.b_b2, (long long)g.b_b3, (long long)g.b_sg, (long long)g.c_rs,
+            (long long)g.c_cs, (long long)g.c_b1, (long long)g.c_b2, (long long)g.c_b3, g.beta);
   GPFVM_CHECK(g.K > 0 && g.nseg > 0, GPFVM_ERR_INVALID, "run_gemm: K and nseg must be positive");
   const bool fast = (g.a_cs == 1) && (g.c_cs == 1) && (g.b_cs == 1 || g.b_rs == 1) && g.M >= 8 &&
                     g.N >= 8 && g.K * g.nseg >= 4;

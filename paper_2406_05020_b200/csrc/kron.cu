@@ -72,6 +72,25 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
   if (P == 0) return;
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
   const int first = rev ? d - 1 : 0;
+  mid_thin = (d == 3 && nout[1] == 1 && nin[1] > 1 && P <= 8 && !getenv("GPFVM_NO_MIDTHIN"));
+  if (mid_thin) {
+    // stk[1]: P functionals (1 x n'_1) stacked as P x n'_1; stk[0]: P time
+    // factors c_p F0^p back to back; stk[2]: F2^p columns concatenated (p, k2)
+    stk[0].ensure((size_t)P * nout[0] * nin[0]);
+    stk[1].ensure((size_t)P * nin[1]);
+    stk[2].ensure((size_t)nout[2] * nin[2] * P);
+    for (int p = 0; p < P; p++) {
+      scaled_copy_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr + (int64_t)p * nout[0] * nin[0],
+                                                                         factors[p][0], coefs[p],
+                                                                         (int64_t)nout[0] * nin[0]);
+      scaled_copy_kernel<<<gsz(nin[1]), 256, 0, s>>>(stk[1].ptr + (int64_t)p * nin[1], factors[p][1], 1.0, nin[1]);
+      restack_kernel<<<gsz((int64_t)nout[2] * nin[2]), 256, 0, s>>>(stk[2].ptr, factors[p][2], 1.0, p, P, nout[2],
+                                                                     nin[2], 1);
+      count_launch(3);
+    }
+    check_launch("KronSum::build (mid-thin)");
+    return;
+  }
   if (d == 2) {
     // plain-GEMM layouts: forward: stk0 rows interleaved (j0,p) with c_p,
     // stk1 columns concatenated (p,k); reverse: stk1 blocks (p,j1) with c_p, stk0 columns
@@ -152,6 +171,7 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
 
 int64_t KronSum::workspace_per_rhs() const {
   if (P == 0 || d == 1) return 0;
+  if (mid_thin) return (int64_t)std::max(nin[0], nout[0]) * P * nin[2];
   int64_t mx = 0;
   for (int s = 0; s <= d - 2; s++) {
     int64_t sz = P;
@@ -166,6 +186,9 @@ int64_t KronSum::workspace_per_rhs() const {
 
 double KronSum::flops_per_rhs() const {
   if (P == 0) return 0.0;
+  if (mid_thin)
+    return 2.0 * P * ((double)nin[0] * nin[1] * nin[2] + (double)nout[0] * nin[0] * nin[2] +
+                      (double)nout[0] * nout[2] * nin[2]);
   if (d == 3 && !rev && Q0 > 0)
     return 2.0 * ((double)Q0 * nout[0] * nin[0] * nin[1] * nin[2] + (double)P * nout[0] * nout[1] * nin[1] * nin[2] +
                   (double)Q2 * nout[0] * nout[1] * nout[2] * nin[2]);
@@ -207,6 +230,37 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     return;
   }
   const int l = d - 1;
+  if (mid_thin) {
+    // A: R[r][a][p][k2] = sum_k1 f_p[k1] X_r[a][k1][k2]   (few-row GEMM over row-major slices)
+    const int64_t rsz = (int64_t)nin[0] * P * nin[2], zsz = (int64_t)nout[0] * P * nin[2];
+    Gemm ga;
+    ga.M = P; ga.N = nin[2]; ga.K = nin[1];
+    ga.A = stk[1].ptr; ga.a_rs = nin[1]; ga.a_cs = 1;
+    ga.B = x; ga.b_rs = nin[2]; ga.b_cs = 1; ga.b_b1 = (int64_t)nin[1] * nin[2]; ga.b_b2 = ldx;
+    ga.C = w0; ga.c_rs = nin[2]; ga.c_cs = 1; ga.c_b1 = (int64_t)P * nin[2]; ga.c_b2 = rsz;
+    ga.batch1 = nin[0]; ga.batch2 = R;
+    run_gemm(ga, s);
+    // B: Z[r][j0][p][k2] = sum_a c_p F0^p[j0][a] R[r][a][p][k2]   (per term)
+    for (int p = 0; p < P; p++) {
+      Gemm gb;
+      gb.M = nout[0]; gb.N = nin[2]; gb.K = nin[0];
+      gb.A = stk[0].ptr + (int64_t)p * nout[0] * nin[0]; gb.a_rs = nin[0]; gb.a_cs = 1;
+      gb.B = w0 + (int64_t)p * nin[2]; gb.b_rs = (int64_t)P * nin[2]; gb.b_cs = 1; gb.b_b1 = rsz;
+      gb.C = w1 + (int64_t)p * nin[2]; gb.c_rs = (int64_t)P * nin[2]; gb.c_cs = 1; gb.c_b1 = zsz;
+      gb.batch1 = R;
+      run_gemm(gb, s);
+    }
+    // C: Y_r[j0][j2] = beta Y + sum_(p,k2) Z[r][j0][(p,k2)] F2^p[j2][k2]
+    Gemm gc;
+    gc.M = nout[0]; gc.N = nout[2]; gc.K = P * nin[2];
+    gc.A = w1; gc.a_rs = (int64_t)P * nin[2]; gc.a_cs = 1; gc.a_b1 = zsz;
+    gc.B = stk[2].ptr; gc.b_rs = 1; gc.b_cs = (int64_t)P * nin[2];
+    gc.C = y; gc.c_rs = nout[2]; gc.c_cs = 1; gc.c_b1 = ldy;
+    gc.batch1 = R;
+    gc.beta = beta;
+    run_gemm(gc, s);
+    return;
+  }
   if (d == 2) {
     const int64_t z0 = (int64_t)P * (rev ? nin[0] * nout[1] : nout[0] * nin[1]);
     Gemm g0, g1;

@@ -43,6 +43,10 @@ struct KronSum {
   // the stage-0 (stage-2) slice: Q0 / Q2 distinct factors, u0[p] / u2[p] map
   int Q0 = 0, Q2 = 0;
   std::vector<int> u0, u2;
+  // 3D with a single output site in the middle dimension (e.g. a boundary face
+  // y = const observed from the PDE block): contract that dimension first (the
+  // cheap, shrinking point functional), then time, then the last dimension
+  bool mid_thin = false;
   void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
              const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
   int64_t workspace_per_rhs() const;
