@@ -45,6 +45,16 @@ __global__ void restack_kernel(double* dst, const double* __restrict__ src, doub
   }
 }
 
+// dst[p][r][i] = src[r][i][p]   (p-innermost -> p-outermost, R x n x P)
+__global__ void p_outer_kernel(double* __restrict__ dst, const double* __restrict__ src, int R, int64_t n, int P) {
+  const int64_t total = (int64_t)R * n * P;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = o / ((int64_t)R * n), rem = o - p * R * n;
+    const int64_t r = rem / n, i = rem - r * n;
+    dst[o] = src[(r * n + i) * P + p];
+  }
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -73,6 +83,25 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
   const int first = rev ? d - 1 : 0;
   mid_thin = (d == 3 && nout[1] == 1 && nin[1] > 1 && P <= 8 && !getenv("GPFVM_NO_MIDTHIN"));
+  last_thin = (!mid_thin && d == 3 && nout[2] == 1 && nin[2] > 1 && nout[1] > 1 && P <= 8 && !getenv("GPFVM_NO_MIDTHIN"));
+  if (last_thin) {
+    // stk[2]: P functionals (1 x n'_2) as a column-major B (P x n'_2); stk[1]:
+    // P factors F1^p back to back; stk[0]: c_p F0^p back to back (K-segments)
+    stk[0].ensure((size_t)P * nout[0] * nin[0]);
+    stk[1].ensure((size_t)P * nout[1] * nin[1]);
+    stk[2].ensure((size_t)P * nin[2]);
+    for (int p = 0; p < P; p++) {
+      scaled_copy_kernel<<<gsz((int64_t)nout[0] * nin[0]), 256, 0, s>>>(stk[0].ptr + (int64_t)p * nout[0] * nin[0],
+                                                                         factors[p][0], coefs[p],
+                                                                         (int64_t)nout[0] * nin[0]);
+      scaled_copy_kernel<<<gsz((int64_t)nout[1] * nin[1]), 256, 0, s>>>(stk[1].ptr + (int64_t)p * nout[1] * nin[1],
+                                                                         factors[p][1], 1.0, (int64_t)nout[1] * nin[1]);
+      scaled_copy_kernel<<<gsz(nin[2]), 256, 0, s>>>(stk[2].ptr + (int64_t)p * nin[2], factors[p][2], 1.0, nin[2]);
+      count_launch(3);
+    }
+    check_launch("KronSum::build (last-thin)");
+    return;
+  }
   if (mid_thin) {
     // stk[1]: P functionals (1 x n'_1) stacked as P x n'_1; stk[0]: P time
     // factors c_p F0^p back to back; stk[2]: F2^p columns concatenated (p, k2)
@@ -172,6 +201,7 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
 int64_t KronSum::workspace_per_rhs() const {
   if (P == 0 || d == 1) return 0;
   if (mid_thin) return (int64_t)std::max(nin[0], nout[0]) * P * nin[2];
+  if (last_thin) return (int64_t)nin[0] * P * std::max(nin[1], nout[1]);
   int64_t mx = 0;
   for (int s = 0; s <= d - 2; s++) {
     int64_t sz = P;
@@ -189,6 +219,9 @@ double KronSum::flops_per_rhs() const {
   if (mid_thin)
     return 2.0 * P * ((double)nin[0] * nin[1] * nin[2] + (double)nout[0] * nin[0] * nin[2] +
                       (double)nout[0] * nout[2] * nin[2]);
+  if (last_thin)
+    return 2.0 * P * ((double)nin[0] * nin[1] * nin[2] + (double)nin[0] * nout[1] * nin[1] +
+                      (double)nout[0] * nin[0] * nout[1]);
   if (d == 3 && !rev && Q0 > 0)
     return 2.0 * ((double)Q0 * nout[0] * nin[0] * nin[1] * nin[2] + (double)P * nout[0] * nout[1] * nin[1] * nin[2] +
                   (double)Q2 * nout[0] * nout[1] * nout[2] * nin[2]);
@@ -256,6 +289,40 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     gc.A = w1; gc.a_rs = (int64_t)P * nin[2]; gc.a_cs = 1; gc.a_b1 = zsz;
     gc.B = stk[2].ptr; gc.b_rs = 1; gc.b_cs = (int64_t)P * nin[2];
     gc.C = y; gc.c_rs = nout[2]; gc.c_cs = 1; gc.c_b1 = ldy;
+    gc.batch1 = R;
+    gc.beta = beta;
+    run_gemm(gc, s);
+    return;
+  }
+  if (last_thin) {
+    const int64_t rows = (int64_t)nin[0] * nin[1];
+    // A: T[r][(a,k1)][p] = sum_k2 X_r[(a,k1)][k2] f_p[k2]   (few-column GEMM, X read once)
+    Gemm ga;
+    ga.M = (int)rows; ga.N = P; ga.K = nin[2];
+    ga.A = x; ga.a_rs = nin[2]; ga.a_cs = 1; ga.a_b1 = ldx;
+    ga.B = stk[2].ptr; ga.b_rs = 1; ga.b_cs = nin[2];
+    ga.C = w1; ga.c_rs = P; ga.c_cs = 1; ga.c_b1 = rows * P;
+    ga.batch1 = R;
+    run_gemm(ga, s);
+    // p outermost: T'[p][r][(a,k1)]
+    p_outer_kernel<<<gsz(rows * R * P), 256, 0, s>>>(w0, w1, R, rows, P);
+    count_launch();
+    // B: U[p][(r,a)][j1] = sum_k1 T'[p][(r,a)][k1] F1^p[j1][k1]   (per term)
+    const int64_t usz = (int64_t)R * nin[0] * nout[1];
+    for (int p = 0; p < P; p++) {
+      Gemm gb;
+      gb.M = R * nin[0]; gb.N = nout[1]; gb.K = nin[1];
+      gb.A = w0 + (int64_t)p * R * rows; gb.a_rs = nin[1]; gb.a_cs = 1;
+      gb.B = stk[1].ptr + (int64_t)p * nout[1] * nin[1]; gb.b_rs = 1; gb.b_cs = nin[1];
+      gb.C = w1 + (int64_t)p * usz; gb.c_rs = nout[1]; gb.c_cs = 1;
+      run_gemm(gb, s);
+    }
+    // C: Y_r[j0][j1] = beta Y + sum_(p,a) c_p F0^p[j0][a] U[p][r][a][j1]   (K-segments over p)
+    Gemm gc;
+    gc.M = nout[0]; gc.N = nout[1]; gc.K = nin[0]; gc.nseg = P;
+    gc.A = stk[0].ptr; gc.a_rs = nin[0]; gc.a_cs = 1; gc.a_sg = (int64_t)nout[0] * nin[0];
+    gc.B = w1; gc.b_rs = nout[1]; gc.b_cs = 1; gc.b_sg = usz; gc.b_b1 = (int64_t)nin[0] * nout[1];
+    gc.C = y; gc.c_rs = nout[1]; gc.c_cs = 1; gc.c_b1 = ldy;
     gc.batch1 = R;
     gc.beta = beta;
     run_gemm(gc, s);

@@ -47,6 +47,9 @@ struct KronSum {
   // y = const observed from the PDE block): contract that dimension first (the
   // cheap, shrinking point functional), then time, then the last dimension
   bool mid_thin = false;
+  // 3D with a single output site in the last dimension (faces x = const of a
+  // (t, y, x) layout): point functional first, then dimension 1, then time
+  bool last_thin = false;
   void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
              const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
   int64_t workspace_per_rhs() const;
