@@ -18,6 +18,8 @@
 //
 // The lag d = e - e' is formed exactly (two_sum) and everything after it is
 // double-double; one rounding at the end.  One thread per entry.
+#include <vector>
+
 #include "internal.h"
 
 namespace gpfvm {
@@ -101,70 +103,133 @@ __device__ static dd g_eval(const MaternDD& K, int o, const dd* poly, dd B0, dd 
   return dd_add(dd_sub(dd_mul(B0, ad), C0), dd_mul(e, p));
 }
 
-__global__ void factor_kernel(MaternDD K, int kindL, const double* __restrict__ loL,
-                              const double* __restrict__ hiL, int nL, int mL, int kindR,
-                              const double* __restrict__ loR, const double* __restrict__ hiR, int nR,
-                              int mR, double* __restrict__ out, int64_t ld) {
-  // the polynomial of g_o and B(0), C(0) depend only on (K, o): one thread per
-  // CTA computes them (dd divisions) into shared memory, bitwise the same
-  // values every thread computed before
-  const int o_blk = (kindL == GPFVM_SITE_POINT ? mL : mL - 1) + (kindR == GPFVM_SITE_POINT ? mR : mR - 1);
-  __shared__ dd s_poly[4], s_B0, s_C0;
+struct FactorArgs {
+  MaternDD K;
+  int kindL, nL, mL, kindR, nR, mR;
+  const double *loL, *hiL, *loR, *hiR;
+};
+
+// per-(K, o) constants: the polynomial of g_o and B(0), C(0) (dd divisions),
+// computed once per CTA into shared memory
+__device__ __forceinline__ void factor_consts(const FactorArgs& a, dd* s_poly, dd& s_B0, dd& s_C0) {
+  const int o_blk = (a.kindL == GPFVM_SITE_POINT ? a.mL : a.mL - 1) + (a.kindR == GPFVM_SITE_POINT ? a.mR : a.mR - 1);
   if (threadIdx.x == 0) {
     dd pl[4];
-    g_poly(K, o_blk, pl);
+    g_poly(a.K, o_blk, pl);
     for (int k = 0; k < 4; k++) s_poly[k] = pl[k];
     s_B0 = dd_make(0.0);
     s_C0 = dd_make(0.0);
     if (o_blk < 0) {
       dd t[4];
-      g_poly(K, -1, t);
+      g_poly(a.K, -1, t);
       s_B0 = t[0];
-      g_poly(K, -2, t);
+      g_poly(a.K, -2, t);
       s_C0 = t[0];
     }
   }
   __syncthreads();
-  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)nL * nR) return;
-  int j = (int)(idx / nR);
-  int jj = (int)(idx % nR);
+}
+
+// F[j][jj]: the 1D functional pair of Eq. 16 as endpoint sums of g_o (R2)
+__device__ double factor_entry(const FactorArgs& a, const dd* s_poly, dd B0, dd C0, int j, int jj) {
   double eL[2], wL[2], eR[2], wR[2];
   int cL, cR, oL, oR;
-  if (kindL == GPFVM_SITE_POINT) {
-    eL[0] = loL[j]; wL[0] = 1.0; cL = 1; oL = mL;
+  if (a.kindL == GPFVM_SITE_POINT) {
+    eL[0] = a.loL[j]; wL[0] = 1.0; cL = 1; oL = a.mL;
   } else {
-    eL[0] = hiL[j]; wL[0] = 1.0; eL[1] = loL[j]; wL[1] = -1.0; cL = 2; oL = mL - 1;
+    eL[0] = a.hiL[j]; wL[0] = 1.0; eL[1] = a.loL[j]; wL[1] = -1.0; cL = 2; oL = a.mL - 1;
   }
-  if (kindR == GPFVM_SITE_POINT) {
-    eR[0] = loR[jj]; wR[0] = 1.0; cR = 1; oR = mR;
+  if (a.kindR == GPFVM_SITE_POINT) {
+    eR[0] = a.loR[jj]; wR[0] = 1.0; cR = 1; oR = a.mR;
   } else {
-    eR[0] = hiR[jj]; wR[0] = 1.0; eR[1] = loR[jj]; wR[1] = -1.0; cR = 2; oR = mR - 1;
+    eR[0] = a.hiR[jj]; wR[0] = 1.0; eR[1] = a.loR[jj]; wR[1] = -1.0; cR = 2; oR = a.mR - 1;
   }
   const int o = oL + oR;
   dd poly[4];
   for (int k = 0; k < 4; k++) poly[k] = s_poly[k];
-  const dd B0 = s_B0, C0 = s_C0;
   dd acc = dd_make(0.0);
-  for (int a = 0; a < cL; a++)
-    for (int b = 0; b < cR; b++) {
-      dd d = two_sum(eL[a], -eR[b]);
-      dd v = g_eval(K, o, poly, B0, C0, d);
-      acc = dd_add(acc, dd_mul_d(v, wL[a] * wR[b]));
+  for (int x = 0; x < cL; x++)
+    for (int y = 0; y < cR; y++) {
+      dd d = two_sum(eL[x], -eR[y]);
+      dd v = g_eval(a.K, o, poly, B0, C0, d);
+      acc = dd_add(acc, dd_mul_d(v, wL[x] * wR[y]));
     }
   double r = dd_to_double(acc);
   if (oR & 1) r = -r;  // (-1)^{o'} (o' = -1 is odd)
-  out[(int64_t)j * ld + jj] = r;
+  return r;
+}
+
+__global__ void factor_kernel(FactorArgs a, double* __restrict__ out, int64_t ld) {
+  __shared__ dd s_poly[4], s_B0, s_C0;
+  factor_consts(a, s_poly, s_B0, s_C0);
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)a.nL * a.nR) return;
+  const int j = (int)(idx / a.nR), jj = (int)(idx % a.nR);
+  out[(int64_t)j * ld + jj] = factor_entry(a, s_poly, s_B0, s_C0, j, jj);
+}
+
+// Uniform site lists (every endpoint sequence arithmetic with one common step,
+// checked exactly on the host): the entry depends only on the lag j - jj — the
+// exact endpoint differences, hence the double-double inputs of g_o, are the
+// same — so one evaluation per lag (nL + nR - 1 instead of nL nR), bitwise
+// equal to the per-entry kernel.
+__global__ void factor_lag_kernel(FactorArgs a, double* __restrict__ lagv) {
+  __shared__ dd s_poly[4], s_B0, s_C0;
+  factor_consts(a, s_poly, s_B0, s_C0);
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;  // lag + nR - 1
+  if (l >= a.nL + a.nR - 1) return;
+  const int lag = l - (a.nR - 1);
+  const int j = lag > 0 ? lag : 0, jj = j - lag;
+  lagv[l] = factor_entry(a, s_poly, s_B0, s_C0, j, jj);
+}
+
+__global__ void lag_fill_kernel(const double* __restrict__ lagv, int nL, int nR, double* __restrict__ out, int64_t ld) {
+  const int64_t total = (int64_t)nL * nR;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx / nR), jj = (int)(idx % nR);
+    out[(int64_t)j * ld + jj] = lagv[j - jj + nR - 1];
+  }
+}
+
+// exact arithmetic-progression test of a site list's endpoints with step h
+bool arithmetic(const std::vector<double>& v, double h) {
+  for (size_t j = 1; j < v.size(); j++)
+    if (v[j] - v[j - 1] != h || v[0] + (double)j * h != v[j]) return false;
+  return true;
+}
+bool uniform_pair(const Sites& L, const Sites& R) {
+  double h = 0.0;
+  if (L.n >= 2) h = L.lo[1] - L.lo[0];
+  else if (R.n >= 2) h = R.lo[1] - R.lo[0];
+  else return false;
+  if (!(h > 0.0)) return false;
+  for (const Sites* S : {&L, &R}) {
+    if (!arithmetic(S->lo, h)) return false;
+    if (S->kind != GPFVM_SITE_POINT && !arithmetic(S->hi, h)) return false;
+  }
+  return true;
 }
 
 void launch_factor(const MaternDD& K, const Sites& L, int mL, const Sites& R, int mR, double* out,
                    int64_t ld, cudaStream_t s) {
   int64_t n = (int64_t)L.n * R.n;
   if (n == 0) return;
+  FactorArgs a{K, L.kind, L.n, mL, R.kind, R.n, mR, L.d_lo.ptr, L.d_hi.ptr, R.d_lo.ptr, R.d_hi.ptr};
+  static const bool no_lag = getenv("GPFVM_NO_LAG") != nullptr;
+  if (!no_lag && n >= 256 && uniform_pair(L, R)) {
+    const int nl = L.n + R.n - 1;
+    DevBuf& lagv = scratch(s, 6);
+    lagv.ensure((size_t)nl);
+    factor_lag_kernel<<<(nl + 127) / 128, 128, 0, s>>>(a, lagv.ptr);
+    lag_fill_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(lagv.ptr, L.n, R.n, out, ld);
+    count_launch(2);
+    check_launch("factor_lag_kernel");
+    return;
+  }
   int threads = 128;
   int64_t blocks = (n + threads - 1) / threads;
-  factor_kernel<<<(unsigned)blocks, threads, 0, s>>>(K, L.kind, L.d_lo.ptr, L.d_hi.ptr, L.n, mL, R.kind,
-                                                    R.d_lo.ptr, R.d_hi.ptr, R.n, mR, out, ld);
+  factor_kernel<<<(unsigned)blocks, threads, 0, s>>>(a, out, ld);
   count_launch();
   check_launch("factor_kernel");
 }
