@@ -217,6 +217,25 @@ def bench_config(builder, R, dev, peak, traffic, world, solve_budget=0):
                         "rel_residual": rep["rel_residual"], "true_rel_residual": rep["true_rel_residual"],
                         "solve_s": e0.elapsed_time(e1) / 1e3, "reorth": "full", "actions_kept": rep["iterations"],
                         "precond": "block-Jacobi FD (DESIGN.md 5.4)"}
+        rb = p.meta.get("rhs_batch")
+        if rb is not None and len(rb) > 1:
+            # the 4-RHS batch (BASELINE configs[2]) through gpfvm_solve_many: one
+            # IterGP run per RHS sharing the batched preconditioner and matvec;
+            # the PCG recurrence (reorth_window=1) over the same budget
+            Yb = torch.tensor(np.ascontiguousarray(rb), dtype=torch.float64, device=dev)
+            Ab = torch.empty_like(Yb)
+            gp.gpfvm_solve(Yb, rtol=1e-8, max_iter=2, out=Ab, reorth_window=1, keep_actions=False)
+            torch.cuda.synchronize()
+            e0.record()
+            _, reps = gp.gpfvm_solve(Yb, rtol=1e-8, max_iter=solve_budget, out=Ab, reorth_window=1,
+                                     keep_actions=False)
+            e1.record()
+            torch.cuda.synchronize()
+            out["solve_batch"] = {"nrhs": len(rb), "budget": solve_budget, "reorth": "window 1 (PCG recurrence)",
+                                  "solve_s": e0.elapsed_time(e1) / 1e3,
+                                  "iterations": [r["iterations"] for r in reps],
+                                  "true_rel_residual": [r["true_rel_residual"] for r in reps]}
+            del Yb, Ab
         del y, alpha
     del gp, X, Y
     torch.cuda.empty_cache()

@@ -196,7 +196,7 @@ int gpfvm_vmul(double* x, const double* d, int64_t n, void* stream);
  * Stops when ||r||_2 <= rtol ||y||_2 (recursive residual) or after
  * max_iter iterations; the report holds the final true residual too.
  * opts may be NULL (defaults below); y, alpha: N-vectors (device or host).
- * nrhs must be 1 (multi-RHS systems: call once per column).  Errors:
+ * One right-hand side (several: gpfvm_solve_many).  Errors:
  * GPFVM_ERR_STATE before assembly, GPFVM_ERR_NUMERIC if the Schur complement
  * cannot be factorised even after shifting, GPFVM_ERR_CUDA on device errors
  * (e.g. out of memory for the Krylov store: see keep_actions). */
@@ -229,6 +229,14 @@ typedef struct {
 
 int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_solve_opts* opts,
                 gpfvm_solve_report* report, void* stream);
+/* nrhs right-hand sides at once (y, alpha: nrhs vectors of stride ld >= N,
+ * device pointers): one IterGP run per right-hand side sharing the batched
+ * preconditioner and Gram matvec (e.g. BASELINE config 2's 4-RHS batch; the N*
+ * solves of a covariance, P:l.288).  reports: nrhs entries.  With the exact 2D
+ * preconditioner the solves run one after the other.  The Krylov store kept
+ * for gpfvm_predict's ITERGP variance is that of right-hand side 0. */
+int gpfvm_solve_many(gpfvm_problem* p, const double* y, double* alpha, int nrhs, int64_t ld,
+                     const gpfvm_solve_opts* opts, gpfvm_solve_report* reports, void* stream);
 
 /* ---- §8 row 4: predict -----------------------------------------------------
  * Posterior on the tensor grid  X_* = pts[0] x ... x pts[ndim-1]  for

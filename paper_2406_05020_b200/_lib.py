@@ -69,6 +69,8 @@ EXPORTS = {
     "gpfvm_gram_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
     "gpfvm_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts),
                               C.POINTER(SolveReport), C.c_void_p]),
+    "gpfvm_solve_many": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.POINTER(SolveOpts),
+                                   C.POINTER(SolveReport), C.c_void_p]),
     "gpfvm_predict": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                 C.c_void_p]),
     "gpfvm_kron_matvec": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_double),

@@ -144,6 +144,16 @@ class GpfvmProblem:
         if out is None:
             out = torch.empty_like(y) if _is_torch(y) else np.empty_like(y)
         opts = L.SolveOpts(float(rtol), int(max_iter), int(precond), int(reorth_window), int(bool(keep_actions)))
+        if y.ndim == 2:  # several right-hand sides (rows): gpfvm_solve_many, device tensors
+            nrhs = int(y.shape[0])
+            if not (_is_torch(y) and y.is_cuda and _is_torch(out) and out.is_cuda):
+                raise ValueError("several right-hand sides: CUDA tensors only")
+            if y.shape[-1] != self.N:
+                raise ValueError(f"y: last dimension {y.shape[-1]}, expected N = {self.N}")
+            reps = (L.SolveReport * nrhs)()
+            L.check(self.lib.gpfvm_solve_many(self.handle, _ptr(y, nrhs * self.N, "y"), _ptr(out, nrhs * self.N, "out"),
+                                              nrhs, int(self.N), C.byref(opts), reps, _stream_of(y)))
+            return out, [{f: getattr(r, f) for f, _ in L.SolveReport._fields_} for r in reps]
         rep = L.SolveReport()
         L.check(self.lib.gpfvm_solve(self.handle, _ptr(y, self.N, "y"), _ptr(out, self.N, "out"), C.byref(opts),
                                      C.byref(rep), _stream_of(y)))

@@ -181,6 +181,22 @@ void build_block_fd(gpfvm_problem* p, int J, BlockFD& bf, cudaStream_t s, Pencil
   GPFVM_CUDA(cudaStreamSynchronize(s));
 }
 
+__global__ void vmul_many(double* x, int64_t ldx, const double* __restrict__ d, int64_t n) {
+  double* xr = x + blockIdx.y * ldx;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    xr[i] *= d[i];
+}
+
+// z_J = Q D^{-1} Q^T r_J for R vectors (strides ldr, ldz); tmp: R * n doubles,
+// w0/w1: R * workspace doubles each (caller-owned)
+void apply_block_fd_many(const BlockFD& bf, const double* r, int64_t ldr, double* z, int64_t ldz, int64_t n, int R,
+                         double* tmp, double* w0, double* w1, cudaStream_t s) {
+  bf.fwd.apply(r, ldr, tmp, n, R, 0.0, w0, w1, s);
+  vmul_many<<<dim3(gsz(n), R), 256, 0, s>>>(tmp, n, bf.Dinv.ptr, n);
+  count_launch();
+  bf.bwd.apply(tmp, n, z, ldz, R, 0.0, w0, w1, s);
+}
+
 // z_J = Q D^{-1} Q^T r_J
 void apply_block_fd(const BlockFD& bf, const double* r, double* z, int64_t n, cudaStream_t s) {
   bf.fwd.apply(r, n, bf.tmp.ptr, n, 1, 0.0, bf.w0.ptr, bf.w1.ptr, s);

@@ -662,6 +662,24 @@ int gpfvm_solve(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
   });
 }
 
+int gpfvm_solve_many(gpfvm_problem* p, const double* y, double* alpha, int nrhs, int64_t ld,
+                     const gpfvm_solve_opts* opts, gpfvm_solve_report* reports, void* stream) {
+  return guarded([&] {
+    GPFVM_CHECK(p && y && alpha && reports, GPFVM_ERR_INVALID, "null argument");
+    GPFVM_CHECK(nrhs >= 1 && ld >= p->N, GPFVM_ERR_INVALID, "nrhs < 1 or ld < N");
+    GPFVM_CHECK(p->assembled, GPFVM_ERR_STATE, "gpfvm_solve_many: call gpfvm_assemble_factors first");
+    GPFVM_CHECK(is_device_ptr(y) && is_device_ptr(alpha), GPFVM_ERR_INVALID, "gpfvm_solve_many: device pointers only");
+    GPFVM_CHECK(y != alpha, GPFVM_ERR_INVALID, "y and alpha must not alias");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    gpfvm_solve_opts o{1e-8, 1000, GPFVM_PRECOND_BLOCK_FD, 0, 1};
+    if (opts) o = *opts;
+    GPFVM_CHECK(o.rtol >= 0 && o.max_iter >= 0 && o.reorth_window >= 0, GPFVM_ERR_INVALID, "bad solve options");
+    cudaStream_t s = (cudaStream_t)stream;
+    solve_many_impl(p, y, ld, alpha, ld, nrhs, o, reports, s);
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int gpfvm_predict(gpfvm_problem* p, const gpfvm_grid* grid, const double* alpha, double* mean, double* var,
                   int cov_mode, void* stream) {
   return guarded([&] {

@@ -242,6 +242,10 @@ void solve_impl(gpfvm_problem* p, const double* y, double* alpha, const gpfvm_so
                 gpfvm_solve_report& rep, cudaStream_t s);
 void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var,
                   int cov_mode, cudaStream_t s);
+void solve_many_impl(gpfvm_problem* p, const double* Y, int64_t ldy, double* X, int64_t ldx, int R,
+                     const gpfvm_solve_opts& o, gpfvm_solve_report* reps, cudaStream_t s);
+void apply_block_fd_many(const BlockFD& bf, const double* r, int64_t ldr, double* z, int64_t ldz, int64_t n, int R,
+                         double* tmp, double* w0, double* w1, cudaStream_t s);
 void destroy_precond(Precond* pc);
 // eigenbases already computed in this preconditioner build, keyed by the
 // pencil's definition: (output, dim, lower order, higher order or -1 for the

@@ -710,21 +710,23 @@ void precond_apply(gpfvm_problem* p, const double* r, double* z, cudaStream_t s)
   }
 }
 
-// grow the Krylov store to `need` slots, keeping the first `valid` ones
-static void ensure_krylov(gpfvm_problem* p, int need, int valid, cudaStream_t s) {
-  Krylov& K = p->kry;
+// grow a Krylov store to `need` slots, keeping the first `valid` ones
+static void ensure_krylov_K(Krylov& K, int64_t N, int need, int valid, cudaStream_t s) {
   if (need <= K.cap) return;
   int cap = std::max(need, std::max(8, K.cap * 2));
   DevBuf d, gd;
-  d.ensure((size_t)cap * p->N);
-  gd.ensure((size_t)cap * p->N);
+  d.ensure((size_t)cap * N);
+  gd.ensure((size_t)cap * N);
   if (valid > 0) {
-    copy(d.ptr, K.d.ptr, (int64_t)valid * p->N, s);
-    copy(gd.ptr, K.gd.ptr, (int64_t)valid * p->N, s);
+    copy(d.ptr, K.d.ptr, (int64_t)valid * N, s);
+    copy(gd.ptr, K.gd.ptr, (int64_t)valid * N, s);
   }
   K.d = std::move(d);
   K.gd = std::move(gd);
   K.cap = cap;
+}
+static void ensure_krylov(gpfvm_problem* p, int need, int valid, cudaStream_t s) {
+  ensure_krylov_K(p->kry, p->N, need, valid, s);
 }
 
 static double norm2(const double* v, int64_t n, double* dtmp, cudaStream_t s) {
@@ -827,6 +829,151 @@ void solve_impl(gpfvm_problem* p, const double* y, double* x, const gpfvm_solve_
   axpy_many(r.ptr, y, N, cdev, -1.0, N, 1, s);  // r = Gx - y
   double tr = norm2(r.ptr, N, cdev + 1, s);
   rep.true_rel_residual = ny > 0 ? tr / ny : 0.0;
+}
+
+// nrhs > 1: one IterGP run per right-hand side, sharing every batched
+// operation: the preconditioner (block-Jacobi FD, R vectors per Kronecker
+// product) and the graph-replayed Gram matvec on R vectors.
+// The per-RHS vector steps run on per-RHS device states, each stopping on its
+// own convergence.  The exact 2D preconditioner is single-vector: those solves
+// run one after the other.  The Krylov store of RHS 0 is the one gpfvm_predict
+// uses for the ITERGP variance.
+void solve_many_impl(gpfvm_problem* p, const double* Y, int64_t ldy, double* X, int64_t ldx, int R,
+                     const gpfvm_solve_opts& o, gpfvm_solve_report* reps, cudaStream_t s) {
+  if (R == 1) {
+    solve_impl(p, Y, X, o, reps[0], s);
+    return;
+  }
+  double t_setup0 = now_ms();
+  const bool had = p->pc != nullptr && p->pc->type == o.precond;
+  build_precond(p, o.precond, s);
+  const double setup_ms = had ? 0.0 : (now_ms() - t_setup0);
+  if (p->pc && !p->pc->blockjacobi) {
+    for (int r = R - 1; r >= 0; r--) {
+      solve_impl(p, Y + r * ldy, X + r * ldx, o, reps[r], s);
+      if (r == R - 1) reps[r].setup_ms = setup_ms;
+    }
+    return;
+  }
+  const int64_t N = p->N;
+  double t0 = now_ms();
+  const bool keep = o.keep_actions != 0;
+  const int W = keep ? 0 : std::max(1, o.reorth_window);
+  const int neta = keep ? std::max(1, o.max_iter) : W;
+  const int64_t sc_per = ST_SIZE + 2 * (int64_t)neta + 8;
+  std::vector<Krylov> extra(R - 1);
+  auto Kr = [&](int r) -> Krylov& { return r == 0 ? p->kry : extra[r - 1]; };
+  p->kry.k = 0;
+  p->kry.eta.clear();
+  DevBuf rv, sc;
+  rv.ensure((size_t)R * N);
+  sc.ensure((size_t)R * sc_per);
+  auto state = [&](int r) { return sc.ptr + r * sc_per; };
+  auto cdev = [&](int r) { return sc.ptr + r * sc_per + ST_SIZE; };
+  auto etad = [&](int r) { return sc.ptr + r * sc_per + ST_SIZE + neta; };
+  for (int r = 0; r < R; r++) {
+    copy(rv.ptr + r * N, Y + r * ldy, N, s);
+    fill(X + r * ldx, 0.0, N, s);
+    itergp_init(Y + r * ldy, N, o.rtol, state(r), s);
+  }
+  std::vector<double> hst((size_t)R * ST_SIZE);
+  auto read_states = [&]() {
+    for (int r = 0; r < R; r++)
+      GPFVM_CUDA(cudaMemcpyAsync(hst.data() + r * ST_SIZE, state(r), ST_SIZE * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+  };
+  auto all_done = [&]() {
+    for (int r = 0; r < R; r++)
+      if (hst[r * ST_SIZE + ST_DONE] == 0.0) return false;
+    return true;
+  };
+  read_states();
+  // batched preconditioner workspaces
+  DevBuf ptmp, pw0, pw1;
+  if (p->pc) {
+    int64_t mx = 1, mw = 1;
+    for (const auto& bf : p->pc->bj) {
+      mx = std::max<int64_t>(mx, p->blocks[bf.J].size);
+      mw = std::max<int64_t>(mw, std::max(bf.fwd.workspace_per_rhs(), bf.bwd.workspace_per_rhs()));
+    }
+    ptmp.ensure((size_t)R * mx);
+    pw0.ensure((size_t)R * mw);
+    pw1.ensure((size_t)R * mw);
+  }
+  p->pcg_s.ensure((size_t)R * N);
+  p->pcg_z.ensure((size_t)R * N);
+  double* d = p->pcg_s.ptr;
+  double* gd = p->pcg_z.ptr;
+  int it = 0;
+  while (it < o.max_iter) {
+    if (it > 0 && (it <= 4 || it % 4 == 0)) {
+      read_states();
+      if (all_done()) break;
+    } else if (it == 0 && all_done()) {
+      break;
+    }
+    const int stored = keep ? it : std::min(it, W);
+    const int slot = keep ? it : it % W;
+    for (int r = 0; r < R; r++) ensure_krylov_K(Kr(r), N, keep ? it + 1 : std::min(it + 1, W), stored, s);
+    if (p->pc) {
+      for (const auto& bf : p->pc->bj) {
+        const BlockInt& B = p->blocks[bf.J];
+        apply_block_fd_many(bf, rv.ptr + B.offset, N, d + B.offset, N, B.size, R, ptmp.ptr, pw0.ptr, pw1.ptr, s);
+      }
+    } else {
+      copy(d, rv.ptr, (int64_t)R * N, s);
+    }
+    matvec_device(p, d, gd, R, N, s);
+    const int w = stored == 0 ? 0 : (keep && o.reorth_window > 0 ? std::min(o.reorth_window, stored) : stored);
+    const int j0 = stored - w;
+    for (int r = 0; r < R; r++) {
+      Krylov& K = Kr(r);
+      double* dr = d + r * N;
+      double* gr = gd + r * N;
+      itergp_reorth_coefs(K.d.ptr + (int64_t)j0 * N, N, w, gr, N, etad(r) + j0, cdev(r), state(r), s);
+      double* dslot = K.d.ptr + (int64_t)slot * N;
+      double* gslot = K.gd.ptr + (int64_t)slot * N;
+      itergp_update(dr, gr, K.d.ptr + (int64_t)j0 * N, K.gd.ptr + (int64_t)j0 * N, N, w, cdev(r), rv.ptr + r * N,
+                    dslot, gslot, N, state(r), etad(r) + slot, s);
+      itergp_step(X + r * ldx, rv.ptr + r * N, dslot, gslot, N, state(r), s);
+    }
+    it++;
+  }
+  read_states();
+  const double iterate_ms = now_ms() - t0;
+  // true residuals: one batched matvec
+  DevBuf res, one;
+  res.ensure((size_t)R * ldx);
+  matvec_device(p, X, res.ptr, R, ldx, s);
+  one.ensure(2);
+  fill(one.ptr, 1.0, 1, s);
+  for (int r = 0; r < R; r++) {
+    axpy_many(res.ptr + r * ldx, Y + r * ldy, N, one.ptr, -1.0, N, 1, s);
+    dot_many(res.ptr + r * ldx, N, res.ptr + r * ldx, N, 1, one.ptr + 1, s);
+    double tr2 = 0.0;
+    GPFVM_CUDA(cudaMemcpyAsync(&tr2, one.ptr + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+    GPFVM_CUDA(cudaStreamSynchronize(s));
+    const double* h = hst.data() + r * ST_SIZE;
+    Krylov& K = Kr(r);
+    const int done_it = (int)h[ST_COUNT];
+    K.k = keep ? done_it : std::min(done_it, W);
+    K.eta.assign(K.k, 0.0);
+    if (K.k > 0) {
+      GPFVM_CUDA(cudaMemcpyAsync(K.eta.data(), etad(r), sizeof(double) * K.k, cudaMemcpyDeviceToHost, s));
+      GPFVM_CUDA(cudaStreamSynchronize(s));
+    }
+    const double ny = h[ST_NY], nr = h[ST_NR];
+    gpfvm_solve_report& rep = reps[r];
+    rep = gpfvm_solve_report{};
+    rep.iterations = done_it;
+    rep.converged = (h[ST_DONE] == 1.0 || ny == 0.0 || (ny > 0 && nr <= o.rtol * ny)) ? 1 : 0;
+    rep.breakdown = h[ST_DONE] == 2.0 ? 1 : 0;
+    rep.rel_residual = ny > 0 ? nr / ny : 0.0;
+    rep.true_rel_residual = ny > 0 ? std::sqrt(tr2) / ny : 0.0;
+    rep.precond_shift = p->pc ? p->pc->shift : 0.0;
+    rep.setup_ms = r == 0 ? setup_ms : 0.0;
+    rep.iterate_ms = iterate_ms;
+  }
 }
 
 }  // namespace gpfvm

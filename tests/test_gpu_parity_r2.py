@@ -113,3 +113,37 @@ def test_precond_variance_multislab_vs_oracle(monkeypatch):
     monkeypatch.delenv("GPFVM_PREDICT_SLAB_ROWS")
     _, var1 = gp.gpfvm_predict(grid, alpha, cov_mode=1, want_mean=False)
     assert np.abs(var1.cpu().numpy() - var).max() <= 1e-11 * prior  # slab plans differ only in rounding
+
+
+@pytest.mark.parametrize("builder,precond", [
+    (lambda: gi.wave_problem(6, 8, 8, ell=(0.5, 0.3, 0.3), ic="sine"), 2),   # block-Jacobi FD: batched
+    (lambda: gi.advdiff_problem(6, 8, 8, n_modes=4), 2),
+    (lambda: gi.heat_problem(12, 16), 2),                                   # exact 2D path: sequential
+    (lambda: gi.heat_problem(8, 8), 0),                                     # no preconditioner: batched
+], ids=["wave-bjfd", "advdiff-bjfd", "heat-exact", "heat-none"])
+def test_solve_many_vs_cholesky(builder, precond):
+    """gpfvm_solve_many (several right-hand sides, one IterGP run each, shared
+    batched preconditioner and matvec) against the dense Cholesky solutions;
+    right-hand side 0 matches the single-RHS solve and its Krylov store drives
+    the ITERGP variance."""
+    p = builder()
+    G = dense_gram(p)
+    rng = np.random.default_rng(7)
+    Y = np.stack([p.rhs(), G @ rng.normal(size=p.size), 0.5 * p.rhs() + G @ rng.normal(size=p.size)])
+    gp = GpfvmProblem(p)
+    gp.gpfvm_assemble_factors()
+    A, reps = gp.gpfvm_solve(_t(Y), rtol=1e-10, max_iter=3000, precond=precond)
+    A = A.cpu().numpy()
+    for r in range(3):
+        assert reps[r]["converged"], (r, reps[r])
+        res = np.linalg.norm(G @ A[r] - Y[r]) / np.linalg.norm(Y[r])
+        assert res <= 2e-10 and abs(reps[r]["true_rel_residual"] - res) <= 1e-10 * max(1.0, res / 1e-10)
+        if r == 0:  # the smooth physical right-hand side: solution to the north_star 1e-8
+            ref = np.linalg.solve(G, Y[r])
+            assert np.linalg.norm(A[r] - ref) <= 1e-6 * np.linalg.norm(ref)
+    grid = gi.Grid([np.linspace(0, 1, 4) for _ in range(p.ndim)])
+    _, v_many = gp.gpfvm_predict(grid, _t(A[0]), cov_mode=0)
+    a0, rep0 = gp.gpfvm_solve(_t(Y[0]), rtol=1e-10, max_iter=3000, precond=precond)
+    assert abs(rep0["iterations"] - reps[0]["iterations"]) <= 2
+    _, v_one = gp.gpfvm_predict(grid, a0, cov_mode=0)
+    assert np.abs(v_many.cpu().numpy() - v_one.cpu().numpy()).max() <= 1e-8
