@@ -370,18 +370,6 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
     count_launch(hit->nodes);
     return;
   }
-  if (no_graph || !hit) {
-    if (!no_graph) {
-      if (pl.graphs.size() >= 16) {
-        if (pl.graphs.front().exec) cudaGraphExecDestroy(pl.graphs.front().exec);
-        pl.graphs.erase(pl.graphs.begin());
-      }
-      pl.graphs.push_back({x, y, nrhs, ld, nullptr, 0, 1});
-    }
-    for (int I = 0; I < nb; I++) matvec_branch(p, I, x, y, nrhs, ld, s);
-    return;
-  }
-  // second sighting: capture
   if (!pl.cap) {
     GPFVM_CUDA(cudaStreamCreateWithFlags(&pl.cap, cudaStreamNonBlocking));
     pl.branch.resize(nb);
@@ -403,17 +391,36 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
     pl.ev.resize(nb + 1);
     for (auto& e : pl.ev) GPFVM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  const int64_t l0 = g_launches.load();
-  cudaGraph_t graph;
-  GPFVM_CUDA(cudaStreamBeginCapture(pl.cap, cudaStreamCaptureModeThreadLocal));
-  try {
-    GPFVM_CUDA(cudaEventRecord(pl.ev[nb], pl.cap));
+  // one branch per output block on its own stream, forked from and joined
+  // into `s` (direct launch) or the capture stream (graph)
+  auto run_branches = [&](cudaStream_t origin) {
+    GPFVM_CUDA(cudaEventRecord(pl.ev[nb], origin));
     for (int I = 0; I < nb; I++) {
       GPFVM_CUDA(cudaStreamWaitEvent(pl.branch[I], pl.ev[nb], 0));
       matvec_branch(p, I, x, y, nrhs, ld, pl.branch[I]);
       GPFVM_CUDA(cudaEventRecord(pl.ev[I], pl.branch[I]));
-      GPFVM_CUDA(cudaStreamWaitEvent(pl.cap, pl.ev[I], 0));
+      GPFVM_CUDA(cudaStreamWaitEvent(origin, pl.ev[I], 0));
     }
+  };
+  if (no_graph || !hit) {
+    if (!no_graph) {
+      if (pl.graphs.size() >= 16) {
+        if (pl.graphs.front().exec) cudaGraphExecDestroy(pl.graphs.front().exec);
+        pl.graphs.erase(pl.graphs.begin());
+      }
+      pl.graphs.push_back({x, y, nrhs, ld, nullptr, 0, 1});
+    }
+    // direct launches on the branch streams: the same streams the capture
+    // uses, so stream-keyed scratch buffers are sized before any capture
+    run_branches(s);
+    return;
+  }
+  // second sighting: capture
+  const int64_t l0 = g_launches.load();
+  cudaGraph_t graph;
+  GPFVM_CUDA(cudaStreamBeginCapture(pl.cap, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_branches(pl.cap);
   } catch (...) {
     cudaStreamEndCapture(pl.cap, &graph);
     throw;
