@@ -310,6 +310,11 @@ int gpfvm_shard_precond_scale(gpfvm_shard* sh, double* z_local, void* stream);
  * gpfvm_shard_create, testable without a GPU. */
 int gpfvm_shard_plan_counts(const gpfvm_problem* p, int rank, int world, int64_t* local_n, int64_t* send1,
                             int64_t* recv1, int64_t* send2, int64_t* recv2);
+/* Sharded posterior mean (Eq. 5, l.113): this rank's partial sum
+ * K_{*,local} alpha_local on the grid (prod(grid->n) doubles, device); the
+ * sum over the ranks (all_reduce) is the mean. */
+int gpfvm_shard_predict_mean(gpfvm_shard* sh, const gpfvm_grid* grid, const double* alpha_local, double* mean_partial,
+                             void* stream);
 /* the local slab of a full (block-concatenated, length N) device vector */
 int gpfvm_shard_gather_local(const gpfvm_shard* sh, const double* full, double* local, void* stream);
 

@@ -98,6 +98,7 @@ EXPORTS = {
     "gpfvm_shard_apply_end": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_shard_precond_scale": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_shard_plan_counts": (C.c_int, [C.c_void_p, C.c_int, C.c_int] + [C.POINTER(C.c_int64)] * 5),
+    "gpfvm_shard_predict_mean": (C.c_int, [C.c_void_p, C.POINTER(Grid), C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_shard_gather_local": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_iter_init": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
     "gpfvm_iter_coefs": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

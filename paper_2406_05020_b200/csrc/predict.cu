@@ -311,6 +311,49 @@ static void var_precond_slab(gpfvm_problem* p, CrossPlan& cp, double* var, int64
   count_launch();
 }
 
+// Time-sharded posterior mean: this rank's share
+//   mean_partial = sum_J K_{*J}[:, owned rows of J] alpha_J,local
+// — the time cross factor restricted to the owned columns; the sum over the
+// ranks (all_reduce by the caller) is the posterior mean of Eq. 5 (l.113).
+// loc_off/row0/rows: the shard layout of every block.
+void predict_mean_shard(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha_local, const int64_t* loc_off,
+                        const int* row0, const int* rows, double* mean, cudaStream_t s) {
+  const int d = p->ndim;
+  int64_t ng = 1;
+  for (int i = 0; i < d; i++) ng *= g.n[i];
+  fill(mean, 0.0, ng, s);
+  CrossPlan cp;
+  build_cross(p, g, 0, g.n[0], cp, s);
+  for (int J = 0; J < (int)p->blocks.size(); J++) {
+    if (cp.terms[J].empty() || rows[J] == 0) continue;
+    const BlockInt& B = p->blocks[J];
+    int in_shape[GPFVM_MAX_DIMS];
+    for (int i = 0; i < d; i++) in_shape[i] = B.shape[i];
+    in_shape[0] = rows[J];
+    std::vector<double> coefs;
+    std::vector<std::vector<const double*>> fs;
+    std::vector<DevBuf> sub(cp.terms[J].size());
+    for (size_t k = 0; k < cp.terms[J].size(); k++) {
+      const KronTerm& t = cp.terms[J][k];
+      const Factor& F0 = cp.factors[t.fid[0]];  // grid_t x n0_J
+      sub[k].ensure((size_t)F0.rows * rows[J]);
+      GPFVM_CUDA(cudaMemcpy2DAsync(sub[k].ptr, rows[J] * sizeof(double), F0.data.ptr + row0[J], F0.cols * sizeof(double),
+                                   rows[J] * sizeof(double), F0.rows, cudaMemcpyDeviceToDevice, s));
+      coefs.push_back(t.coef);
+      std::vector<const double*> f{sub[k].ptr};
+      for (int i = 1; i < d; i++) f.push_back(cp.factors[t.fid[i]].data.ptr);
+      fs.push_back(f);
+    }
+    KronSum ks;
+    ks.build(d, in_shape, cp.gshape, coefs, fs, s);
+    size_t need = (size_t)std::max<int64_t>(1, ks.workspace_per_rhs());
+    cp.w0.ensure(need);
+    cp.w1.ensure(need);
+    ks.apply(alpha_local + loc_off[J], 1, mean, ng, 1, 1.0, cp.w0.ptr, cp.w1.ptr, s);
+    GPFVM_CUDA(cudaStreamSynchronize(s));  // sub / ks freed on scope exit
+  }
+}
+
 void predict_impl(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha, double* mean, double* var, int cov_mode,
                   cudaStream_t s) {
   const int d = p->ndim;

@@ -247,6 +247,8 @@ void solve_many_impl(gpfvm_problem* p, const double* Y, int64_t ldy, double* X, 
 void apply_block_fd_many(const BlockFD& bf, const double* r, int64_t ldr, double* z, int64_t ldz, int64_t n, int R,
                          double* tmp, double* w0, double* w1, cudaStream_t s);
 void destroy_precond(Precond* pc);
+void predict_mean_shard(gpfvm_problem* p, const gpfvm_grid& g, const double* alpha_local, const int64_t* loc_off,
+                        const int* row0, const int* rows, double* mean, cudaStream_t s);
 // eigenbases already computed in this preconditioner build, keyed by the
 // pencil's definition: (output, dim, lower order, higher order or -1 for the
 // identity, site kind) and the site endpoints — blocks that share a site list

@@ -649,6 +649,25 @@ int gpfvm_shard_precond_scale(gpfvm_shard* sh, double* z_local, void* stream) {
   });
 }
 
+int gpfvm_shard_predict_mean(gpfvm_shard* sh, const gpfvm_grid* grid, const double* alpha_local, double* mean_partial,
+                             void* stream) {
+  return guarded_shard([&] {
+    GPFVM_CHECK(sh && grid && alpha_local && mean_partial, GPFVM_ERR_INVALID, "null argument");
+    gpfvm_problem* p = sh->p;
+    GPFVM_CHECK(grid->output >= 0 && grid->output < p->nout, GPFVM_ERR_INVALID, "grid output out of range");
+    for (int i = 0; i < p->ndim; i++)
+      GPFVM_CHECK(grid->n[i] >= 1 && grid->pts[i], GPFVM_ERR_INVALID, "empty grid dimension");
+    GPFVM_CUDA(cudaSetDevice(p->device));
+    std::vector<int> row0(sh->L.nb), rows(sh->L.nb);
+    for (int J = 0; J < sh->L.nb; J++) {
+      row0[J] = sh->L.row0(J, sh->L.rank);
+      rows[J] = sh->L.rows(J, sh->L.rank);
+    }
+    predict_mean_shard(p, *grid, alpha_local, sh->L.loc_off.data(), row0.data(), rows.data(), mean_partial,
+                       (cudaStream_t)stream);
+  });
+}
+
 int gpfvm_shard_gather_local(const gpfvm_shard* sh, const double* full, double* local, void* stream) {
   return guarded_shard([&] {
     GPFVM_CHECK(sh && full && local, GPFVM_ERR_INVALID, "bad arguments");

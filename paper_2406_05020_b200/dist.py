@@ -254,6 +254,23 @@ class ShardedProblem:
                             float(h[ST_NR]) / ny if ny > 0 else 0.0)
         return xs, rep
 
+    # -- posterior mean on a grid (Eq. 5): partial sums per rank + all_reduce
+    def predict_mean(self, grid, alphas):
+        import numpy as np
+        d = self.gps[0].problem.ndim
+        pts = [np.ascontiguousarray(p, dtype=np.float64) for p in grid.points]
+        g = L.Grid()
+        for i in range(d):
+            g.n[i] = int(pts[i].shape[0])
+            g.pts[i] = pts[i].ctypes.data_as(C.POINTER(C.c_double))
+        g.output = int(grid.output)
+        ng = int(np.prod([p.shape[0] for p in pts]))
+        means = [torch.empty(ng, dtype=torch.float64, device=dv) for dv in self.dev]
+        for i, h in enumerate(self.G.h):
+            L.check(self.lib.gpfvm_shard_predict_mean(h, C.byref(g), _p(alphas[i]), _p(means[i]), _stream(self.dev[i])))
+        self.comm.allreduce(means)
+        return means
+
     def close(self):
         self.G.close()
         if self.P is not None:

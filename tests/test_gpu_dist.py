@@ -99,3 +99,23 @@ def test_sharded_solve_matches_single_gpu_iterations(monkeypatch):
     assert rep1["converged"] and rep2.converged
     assert abs(rep1["iterations"] - rep2.iterations) <= 2, (rep1["iterations"], rep2.iterations)
     sp.close()
+
+
+@pytest.mark.parametrize("W", [2, 3])
+def test_sharded_predict_mean(W):
+    """Sharded posterior mean (partial sums over the owned time rows +
+    all_reduce) equals the oracle's Cholesky posterior mean."""
+    from oracle.posterior import posterior_exact
+    p = gi.wave_problem(6, 8, 8, ell=(0.5, 0.3, 0.3), ic="sine")
+    G = dense_gram(p)
+    y = p.rhs()
+    grid = gi.Grid([np.linspace(0, 1, 5), np.linspace(0.1, 0.9, 4), np.linspace(0, 1, 3)])
+    m_ref, _, _ = posterior_exact(p, grid, G, y)
+    sp, gps = _sharded(p, W)
+    yt = torch.tensor(y, device="cuda:0")
+    xs, rep = sp.solve(sp.local([yt] * W), rtol=1e-12, max_iter=600)
+    assert rep.converged
+    means = sp.predict_mean(grid, xs)
+    for m in means:
+        assert np.abs(m.cpu().numpy() - m_ref).max() <= 1e-8 * np.abs(m_ref).max()
+    sp.close()
