@@ -44,6 +44,21 @@ def main():
                  "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over all {len(per)} kernels of "
                            f"one {R}-RHS matvec (tools/matvec_once.py {cfg} {R}; {os.path.basename(path)})"}
     json.dump(data, open(out_path, "w"), indent=1)
+    # per-kernel-name summary (count, serialised time, DRAM bytes, GB/s)
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for i, m in per.items():
+        a = agg[names[i]]
+        a[0] += 1
+        a[1] += m.get("gpu__time_duration.sum", 0)
+        a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+    txt = os.path.join(ROOT, "profiles", f"r02_plan_{cfg}.txt")
+    with open(txt, "w") as f:
+        f.write(f"# {cfg}: one {R}-RHS Gram matvec, every kernel (ncu --metrics dram__bytes_read.sum,"
+                f"dram__bytes_write.sum,gpu__time_duration.sum, serialised, cold-cache; {os.path.basename(path)})\n")
+        f.write(f"# total {tot_t * 1e3:.3f} ms serialised over {len(per)} launches, DRAM {tot_b / 1e6:.1f} MB\n")
+        f.write(f"# {'kernel':<50} {'n':>4} {'time_us':>10} {'share':>7} {'DRAM_MB':>9} {'GB/s':>7}\n")
+        for k, (n, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"{k:<52} {n:>4} {t * 1e6:>10.1f} {100 * t / tot_t:>6.1f}% {b / 1e6:>9.1f} {b / max(t, 1e-12) / 1e9:>7.0f}\n")
     print(cfg, R, f"{tot_b / 1e6:.1f} MB over {len(per)} kernels, {tot_t * 1e3:.3f} ms serialised")
 
 
