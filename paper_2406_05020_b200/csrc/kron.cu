@@ -28,6 +28,12 @@ __global__ void scaled_copy_kernel(double* dst, const double* __restrict__ src, 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = c * src[i];
 }
+// dst = a A + b B
+__global__ void lincomb2_kernel(double* dst, double a, const double* __restrict__ A, double b,
+                                const double* __restrict__ B, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = a * A[i] + b * B[i];
+}
 unsigned gsz(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 2048)); }
 
 // 2D restacking so that both stages are plain GEMMs (no K-segments):
@@ -71,14 +77,43 @@ double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
 }
 }  // namespace
 
-void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
-                    const std::vector<std::vector<const double*>>& factors, cudaStream_t s) {
+void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std::vector<double>& coefs_in,
+                    const std::vector<std::vector<const double*>>& factors_in, cudaStream_t s) {
   d = d_;
-  P = (int)coefs.size();
   for (int i = 0; i < GPFVM_MAX_DIMS; i++) {
     nin[i] = (i < d) ? in_shape[i] : 1;
     nout[i] = (i < d) ? out_shape[i] : 1;
   }
+  // Terms that share every factor but one merge exactly (bilinearity):
+  //   c_p (x)F_p + c_q (x)F_q = (x)F with F_e = c_p F_p,e + c_q F_q,e
+  // e.g. advection-diffusion: (y,y) + (yy,yy) share T00 (x) X00, (x,x) +
+  // (xx,xx) share T00 (.) Y00: 9 -> 7 Kronecker terms.
+  std::vector<double> coefs = coefs_in;
+  std::vector<std::vector<const double*>> factors = factors_in;
+  merged.clear();
+  static const bool no_merge = getenv("GPFVM_NO_MERGE") != nullptr;
+  for (bool again = !no_merge; again;) {
+    again = false;
+    for (size_t a = 0; a < coefs.size() && !again; a++)
+      for (size_t b = a + 1; b < coefs.size() && !again; b++) {
+        int e = -1, ndiff = 0;
+        for (int i = 0; i < d; i++)
+          if (factors[a][i] != factors[b][i]) { e = i; ndiff++; }
+        if (ndiff != 1) continue;
+        const int64_t fs = (int64_t)nout[e] * nin[e];
+        merged.emplace_back();
+        DevBuf& m = merged.back();
+        m.ensure((size_t)fs);
+        lincomb2_kernel<<<gsz(fs), 256, 0, s>>>(m.ptr, coefs[a], factors[a][e], coefs[b], factors[b][e], fs);
+        count_launch();
+        factors[a][e] = m.ptr;
+        coefs[a] = 1.0;
+        coefs.erase(coefs.begin() + b);
+        factors.erase(factors.begin() + b);
+        again = true;
+      }
+  }
+  P = (int)coefs.size();
   if (P == 0) return;
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
   const int first = rev ? d - 1 : 0;

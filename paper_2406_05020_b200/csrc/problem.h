@@ -39,6 +39,7 @@ struct KronSum {
   bool rev = false;  // contraction order: dim d-1 first (chosen by flop count)
   int nin[GPFVM_MAX_DIMS] = {1, 1, 1, 1}, nout[GPFVM_MAX_DIMS] = {1, 1, 1, 1};
   DevBuf stk[GPFVM_MAX_DIMS];  // stacked factors per dim (coefficients folded into dim 0)
+  std::vector<DevBuf> merged;  // combined factors of merged terms (build)
   // 3D forward plain path: terms that share their dim-0 (dim-2) factor share
   // the stage-0 (stage-2) slice: Q0 / Q2 distinct factors, u0[p] / u2[p] map
   int Q0 = 0, Q2 = 0;
