@@ -1,7 +1,8 @@
 // FP64 tensor-core GEMM for the Kronecker mode products:
 // TMA-fed, mbarrier-pipelined, warp-specialised DMMA kernel for sm_100a.
 //
-//   C[b] = alpha * sum_seg A_seg[b] B_seg[b] + beta * C[b]     (one batch level)
+//   C[b] = alpha * sum_seg A_seg[b] B_seg[b] + beta * C[b]     (two batch levels
+//   b = (b1, b2), each operand with its own strides or broadcast per level)
 //
 // FP64 on sm_100a has no tcgen05 kind: the tensor-core instruction is
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4, 256 FMA, one per 16 cycles per SM
@@ -24,7 +25,7 @@
 //     predication in the main loop).
 // Requirements (else the caller uses the generic kernels in gemm.cu): 16-byte
 // aligned base pointers, even element strides, a_cs == c_cs == 1, b_cs == 1 or
-// b_rs == 1, one batch level <= 65535.
+// b_rs == 1, at most two batch levels (the extra term: one).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -44,14 +45,15 @@ namespace {
 
 struct TmaArgs {
   int M, N, batch;
+  int batch1;  // size of batch level 1 (b = b1 + batch1 * b2)
   int kt_seg;  // 16-wide k tiles per segment
   int kt_extra;  // k tiles of the extra term (tmA2 / tmB2), after the segments
   int nseg;
-  int a_bcast, b_bcast;  // operand shared by every batch entry
+  int a_bc1, a_bc2, b_bc1, b_bc2;  // operand shared along batch level 1 / 2
   int dbg;               // debugging switches (GPFVM_TMA_DBG bits)
   double alpha, beta;
   double* C;
-  int64_t c_rs, c_b1;
+  int64_t c_rs, c_b1, c_b2;
 };
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -80,12 +82,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint64_t* bar) {
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-      "[%6];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ double lds64(uint32_t addr) {
@@ -153,25 +155,26 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, MINB)
         const int64_t r = t / tiles_n;
         const int tm = (int)(r % tiles_m), b = (int)(r / tiles_m);
         const int m0 = tm * BM, n0 = tn * BN;
-        const int ba = g.a_bcast ? 0 : b, bb = g.b_bcast ? 0 : b;
+        const int b1 = b % g.batch1, b2 = b / g.batch1;
+        const int a1 = g.a_bc1 ? 0 : b1, a2 = g.a_bc2 ? 0 : b2, bq1 = g.b_bc1 ? 0 : b1, bq2 = g.b_bc2 ? 0 : b2;
         for (int kt = 0; kt < KT; kt++, it++) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           mbar_expect_tx(&full[s], L::A_BYTES + L::B_BYTES);
           if (kt >= KTm) {  // extra low-rank term (same layout class, own maps)
             const int k0 = (kt - KTm) * 16;
-            tma_load_4d(sA + s * L::A_BYTES, &tmA2, k0, m0, 0, b, &full[s]);
-            tma_load_4d(sB + s * L::B_BYTES, &tmB2, k0, n0, 0, b, &full[s]);
+            tma_load_5d(sA + s * L::A_BYTES, &tmA2, k0, m0, 0, b, 0, &full[s]);
+            tma_load_5d(sB + s * L::B_BYTES, &tmB2, k0, n0, 0, b, 0, &full[s]);
             continue;
           }
           const int seg = kt / g.kt_seg, k0 = (kt - seg * g.kt_seg) * 16;
-          tma_load_4d(sA + s * L::A_BYTES, &tmA, k0, m0, seg, ba, &full[s]);
+          tma_load_5d(sA + s * L::A_BYTES, &tmA, k0, m0, seg, a1, a2, &full[s]);
           if (BROW) {
 #pragma unroll
             for (int j = 0; j < BN / 16; j++)
-              tma_load_4d(sB + s * L::B_BYTES + j * 2048, &tmB, n0 + 16 * j, k0, seg, bb, &full[s]);
+              tma_load_5d(sB + s * L::B_BYTES + j * 2048, &tmB, n0 + 16 * j, k0, seg, bq1, bq2, &full[s]);
           } else {
-            tma_load_4d(sB + s * L::B_BYTES, &tmB, k0, n0, seg, bb, &full[s]);
+            tma_load_5d(sB + s * L::B_BYTES, &tmB, k0, n0, seg, bq1, bq2, &full[s]);
           }
         }
       }
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, MINB)
 
     // ---- epilogue: C = alpha acc + beta C (two consecutive doubles per lane);
     // the producer is already filling the ring with the next tile ----
-    double* C = g.C + (int64_t)b * g.c_b1;
+    double* C = g.C + (int64_t)(b % g.batch1) * g.c_b1 + (int64_t)(b / g.batch1) * g.c_b2;
 #pragma unroll
     for (int i = 0; i < TM; i++) {
       const int row = m0 + wm0 + i * 8 + g8;
@@ -283,19 +286,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 4D tiled map over doubles: dims (d0 contiguous, d1, d2, d3) with element strides s1..s3
-bool make_map(CUtensorMap* m, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, int64_t s1,
-              int64_t s2, int64_t s3, uint32_t b0, uint32_t b1) {
+// 5D tiled map over doubles: dims (d0 contiguous, d1, d2, d3, d4) with element strides s1..s4
+bool make_map(CUtensorMap* m, const double* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint64_t d4,
+              int64_t s1, int64_t s2, int64_t s3, int64_t s4, uint32_t b0, uint32_t b1) {
   auto fn = encode_fn();
   if (!fn) return false;
   // size-1 dims: any legal stride
   if (d2 == 1) s2 = std::max<int64_t>(s1, 2);
   if (d3 == 1) s3 = std::max<int64_t>(s2, 2);
-  cuuint64_t dims[4] = {d0, d1, d2, d3};
-  cuuint64_t strides[3] = {(cuuint64_t)s1 * 8, (cuuint64_t)s2 * 8, (cuuint64_t)s3 * 8};
-  cuuint32_t box[4] = {b0, b1, 1, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
+  if (d4 == 1) s4 = std::max<int64_t>(s3, 2);
+  if (s2 <= 0 || s3 <= 0 || s4 <= 0) return false;
+  cuuint64_t dims[5] = {d0, d1, d2, d3, d4};
+  cuuint64_t strides[4] = {(cuuint64_t)s1 * 8, (cuuint64_t)s2 * 8, (cuuint64_t)s3 * 8, (cuuint64_t)s4 * 8};
+  cuuint32_t box[5] = {b0, b1, 1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -350,7 +355,7 @@ bool ev(int64_t v) { return (v & 1) == 0; }
 static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
   static const bool off = getenv("GPFVM_NO_TMA") != nullptr;
   if (off) return false;
-  if (g.batch2 != 1 || g.batch3 != 1) return false;
+  if (g.batch3 != 1 || (g.K2 > 0 && g.batch2 != 1)) return false;
   if (g.a_cs != 1 || g.c_cs != 1) return false;
   const bool brow = (g.b_cs == 1);
   if (!brow && g.b_rs != 1) return false;
@@ -358,38 +363,46 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
   if (!al16(g.A) || !al16(g.B) || !al16(g.C)) return false;
   const int64_t b_ld = brow ? g.b_rs : g.b_cs;
   if (!ev(g.a_rs) || !ev(b_ld) || !ev(g.c_rs) || !ev(g.a_sg) || !ev(g.b_sg) || !ev(g.a_b1) || !ev(g.b_b1) ||
-      !ev(g.c_b1))
+      !ev(g.c_b1) || !ev(g.a_b2) || !ev(g.b_b2) || !ev(g.c_b2))
     return false;
-  const int batch = g.batch1;
+  const int batch = g.batch1 * g.batch2;
+  if ((int64_t)g.batch1 * g.batch2 > (1 << 30)) return false;
   if (g.K2 > 0 && (brow || !al16(g.A2) || !al16(g.B2) || !ev(g.a2_rs) || !ev(g.b2_rs) || !ev(g.a2_b1) ||
                    !ev(g.b2_b1)))
     return false;
-  const bool a_bc = (g.a_b1 == 0) || batch == 1, b_bc = (g.b_b1 == 0) || batch == 1;
+  const bool a_bc1 = (g.a_b1 == 0) || g.batch1 == 1, b_bc1 = (g.b_b1 == 0) || g.batch1 == 1;
+  const bool a_bc2 = (g.a_b2 == 0) || g.batch2 == 1, b_bc2 = (g.b_b2 == 0) || g.batch2 == 1;
   CUtensorMap ma, mb, ma2, mb2;
   memset(&ma2, 0, sizeof(ma2));
   memset(&mb2, 0, sizeof(mb2));
   TmaArgs a;
   a.kt_extra = g.K2 > 0 ? (g.K2 + 15) / 16 : 0;
-  a.M = g.M; a.N = g.N; a.batch = g.batch1;
+  a.M = g.M; a.N = g.N; a.batch = batch; a.batch1 = g.batch1;
   a.kt_seg = (g.K + 15) / 16;
   a.nseg = g.nseg;
-  a.a_bcast = a_bc; a.b_bcast = b_bc;
+  a.a_bc1 = a_bc1; a.a_bc2 = a_bc2; a.b_bc1 = b_bc1; a.b_bc2 = b_bc2;
   a.alpha = g.alpha; a.beta = g.beta;
   static const int dbgbits = getenv("GPFVM_TMA_DBG") ? atoi(getenv("GPFVM_TMA_DBG")) : 0;
   a.dbg = dbgbits;
-  a.C = g.C; a.c_rs = g.c_rs; a.c_b1 = g.c_b1;
+  a.C = g.C; a.c_rs = g.c_rs; a.c_b1 = g.c_b1; a.c_b2 = g.c_b2;
   static const int variant = getenv("GPFVM_TMA_VARIANT") ? atoi(getenv("GPFVM_TMA_VARIANT")) : -1;
   auto run = [&](auto cfg) -> bool {
     using Cfg = decltype(cfg);
-    if (!make_map(&ma, g.A, g.K, g.M, g.nseg, a_bc ? 1 : batch, g.a_rs, g.a_sg, g.a_b1, 16, Cfg::BM)) return false;
+    if (!make_map(&ma, g.A, g.K, g.M, g.nseg, a_bc1 ? 1 : g.batch1, a_bc2 ? 1 : g.batch2, g.a_rs, g.a_sg, g.a_b1,
+                  g.a_b2, 16, Cfg::BM))
+      return false;
     if (brow) {
-      if (!make_map(&mb, g.B, g.N, g.K, g.nseg, b_bc ? 1 : batch, g.b_rs, g.b_sg, g.b_b1, 16, 16)) return false;
+      if (!make_map(&mb, g.B, g.N, g.K, g.nseg, b_bc1 ? 1 : g.batch1, b_bc2 ? 1 : g.batch2, g.b_rs, g.b_sg, g.b_b1,
+                    g.b_b2, 16, 16))
+        return false;
       launch_tma<Cfg::BM, Cfg::BN, Cfg::WMr, Cfg::WNr, Cfg::ST, true, Cfg::MINB>(ma, mb, ma2, mb2, a, batch, s);
     } else {
-      if (!make_map(&mb, g.B, g.K, g.N, g.nseg, b_bc ? 1 : batch, g.b_cs, g.b_sg, g.b_b1, 16, Cfg::BN)) return false;
+      if (!make_map(&mb, g.B, g.K, g.N, g.nseg, b_bc1 ? 1 : g.batch1, b_bc2 ? 1 : g.batch2, g.b_cs, g.b_sg, g.b_b1,
+                    g.b_b2, 16, Cfg::BN))
+        return false;
       if (g.K2 > 0) {
-        if (!make_map(&ma2, g.A2, g.K2, g.M, 1, batch, g.a2_rs, 0, g.a2_b1, 16, Cfg::BM)) return false;
-        if (!make_map(&mb2, g.B2, g.K2, g.N, 1, batch, g.b2_rs, 0, g.b2_b1, 16, Cfg::BN)) return false;
+        if (!make_map(&ma2, g.A2, g.K2, g.M, 1, batch, 1, g.a2_rs, 0, g.a2_b1, 0, 16, Cfg::BM)) return false;
+        if (!make_map(&mb2, g.B2, g.K2, g.N, 1, batch, 1, g.b2_rs, 0, g.b2_b1, 0, 16, Cfg::BN)) return false;
       }
       launch_tma<Cfg::BM, Cfg::BN, Cfg::WMr, Cfg::WNr, Cfg::ST, false, Cfg::MINB>(ma, mb, ma2, mb2, a, batch, s);
     }

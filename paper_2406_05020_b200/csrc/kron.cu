@@ -61,6 +61,81 @@ __global__ void p_outer_kernel(double* __restrict__ dst, const double* __restric
   }
 }
 
+// Reflection-parity split (KronSum::par).  Half blocks of one factor
+// (n x n, h = n/2) for parity class c of the input (0: even part, 1: odd part):
+//   H_c[j][k] = coef * (F[j][k] + (-1)^c F[j][n-1-k])   j, k < h
+// mode 0: dst[c][(j*P + p)][k]   (rows interleaved by term, stage-0 A)
+// mode 1: dst[c][j][p*h + k]     (columns concatenated by term, stage-1 B)
+__global__ void half_restack_kernel(double* dst, const double* __restrict__ F, double coef, int p, int P, int n,
+                                    int mode) {
+  const int h = n / 2;
+  const int64_t tot = 2LL * h * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / ((int64_t)h * h));
+    const int j = (int)((e / h) % h), k = (int)(e % h);
+    const double a = F[(int64_t)j * n + k], b = F[(int64_t)j * n + (n - 1 - k)];
+    const double v = coef * (c ? a - b : a + b);
+    const int64_t o = mode == 0 ? (int64_t)c * P * h * h + ((int64_t)j * P + p) * h + k
+                                : (int64_t)c * h * P * h + (int64_t)j * P * h + (int64_t)p * h + k;
+    dst[o] = v;
+  }
+}
+
+// x (R vectors, n0 x n1 row-major, stride ldx) -> parity classes
+// xt[a][r][b][i][j] (a: time class, b: space class, i < h0, j < h1):
+//   u/v along dim 0 then along dim 1 (sums and differences, no scaling)
+__global__ void parity_fwd2_kernel(const double* __restrict__ x, int64_t ldx, double* __restrict__ xt, int R, int n0,
+                                   int n1) {
+  const int h0 = n0 / 2, h1 = n1 / 2;
+  const int64_t cls = (int64_t)h0 * h1, tot = (int64_t)R * cls;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cls, ij = e - r * cls;
+    const int i = (int)(ij / h1), j = (int)(ij - (int64_t)i * h1);
+    const double* xr = x + r * ldx;
+    const double x00 = xr[(int64_t)i * n1 + j], x01 = xr[(int64_t)i * n1 + (n1 - 1 - j)];
+    const double x10 = xr[(int64_t)(n0 - 1 - i) * n1 + j], x11 = xr[(int64_t)(n0 - 1 - i) * n1 + (n1 - 1 - j)];
+    const double u0 = x00 + x10, u1 = x01 + x11, v0 = x00 - x10, v1 = x01 - x11;
+    xt[((0 * (int64_t)R + r) * 2 + 0) * cls + ij] = u0 + u1;
+    xt[((0 * (int64_t)R + r) * 2 + 1) * cls + ij] = u0 - u1;
+    xt[((1 * (int64_t)R + r) * 2 + 0) * cls + ij] = v0 + v1;
+    xt[((1 * (int64_t)R + r) * 2 + 1) * cls + ij] = v0 - v1;
+  }
+}
+
+// Inverse: y = beta y + (1/4) recombined classes + sum_k U[r][row][k] V[r][col][k]
+// (the optional low-rank IC/BC coupling update).  The class of
+// output parity (a, b) sits at position (a ^ sg0, b ^ sg1) (positions are
+// input classes; a skew factor maps even to odd).
+__global__ void parity_inv2_kernel(const double* __restrict__ yt, double* __restrict__ y, int64_t ldy, int R, int n0,
+                                   int n1, int sg0, int sg1, double beta, const double* __restrict__ U,
+                                   int64_t u_rs, int64_t u_b1, const double* __restrict__ V, int64_t v_rs,
+                                   int64_t v_b1, int rk) {
+  const int h0 = n0 / 2, h1 = n1 / 2;
+  const int64_t cls = (int64_t)h0 * h1, tot = (int64_t)R * cls;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cls, ij = e - r * cls;
+    const int i = (int)(ij / h1), j = (int)(ij - (int64_t)i * h1);
+    auto at = [&](int a, int b) { return yt[(((int64_t)(a ^ sg0) * R + r) * 2 + (b ^ sg1)) * cls + ij]; };
+    const double Y00 = at(0, 0), Y01 = at(0, 1), Y10 = at(1, 0), Y11 = at(1, 1);
+    const int i1 = n0 - 1 - i, j1 = n1 - 1 - j;
+    double o[4] = {0.25 * ((Y00 + Y01) + (Y10 + Y11)), 0.25 * ((Y00 - Y01) + (Y10 - Y11)),
+                   0.25 * ((Y00 + Y01) - (Y10 + Y11)), 0.25 * ((Y00 - Y01) - (Y10 - Y11))};
+    const int rows[4] = {i, i, i1, i1}, cols[4] = {j, j1, j, j1};
+    double* yr = y + r * ldy;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      double v = o[q];
+      if (rk > 0) {
+        const double* u = U + r * u_b1 + (int64_t)rows[q] * u_rs;
+        const double* w = V + r * v_b1 + (int64_t)cols[q] * v_rs;
+        for (int k = 0; k < rk; k++) v = fma(u[k], w[k], v);
+      }
+      double* yp = yr + (int64_t)rows[q] * n1 + cols[q];
+      *yp = (beta != 0.0) ? fma(beta, *yp, v) : v;
+    }
+  }
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -78,7 +153,8 @@ double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
 }  // namespace
 
 void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std::vector<double>& coefs_in,
-                    const std::vector<std::vector<const double*>>& factors_in, cudaStream_t s) {
+                    const std::vector<std::vector<const double*>>& factors_in, cudaStream_t s,
+                    const std::vector<std::vector<int>>* signs_in) {
   d = d_;
   for (int i = 0; i < GPFVM_MAX_DIMS; i++) {
     nin[i] = (i < d) ? in_shape[i] : 1;
@@ -90,6 +166,8 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
   // (xx,xx) share T00 (.) Y00: 9 -> 7 Kronecker terms.
   std::vector<double> coefs = coefs_in;
   std::vector<std::vector<const double*>> factors = factors_in;
+  std::vector<std::vector<int>> signs = signs_in ? *signs_in
+                                                 : std::vector<std::vector<int>>(coefs.size(), std::vector<int>(d, 0));
   merged.clear();
   static const bool no_merge = getenv("GPFVM_NO_MERGE") != nullptr;
   for (bool again = !no_merge; again;) {
@@ -108,13 +186,38 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
         count_launch();
         factors[a][e] = m.ptr;
         coefs[a] = 1.0;
+        if (signs[a][e] != signs[b][e]) signs[a][e] = 0;  // mixed parity: no split
         coefs.erase(coefs.begin() + b);
         factors.erase(factors.begin() + b);
+        signs.erase(signs.begin() + b);
         again = true;
       }
   }
   P = (int)coefs.size();
   if (P == 0) return;
+  // reflection-parity split: every factor of a dimension has the same
+  // nonzero sign, square even-length dimensions
+  static const bool no_par = getenv("GPFVM_NO_KRON_PARITY") != nullptr;
+  par = (d == 2) && !no_par;
+  for (int i = 0; i < d && par; i++) {
+    par = nin[i] == nout[i] && nin[i] >= 2 && nin[i] % 2 == 0 && signs[0][i] != 0;
+    for (int p = 0; p < P && par; p++) par = signs[p][i] == signs[0][i];
+    sg[i] = par ? (signs[0][i] < 0 ? 1 : 0) : 0;
+  }
+  if (par) {
+    rev = false;
+    mid_thin = last_thin = false;
+    const int h0 = nin[0] / 2, h1 = nin[1] / 2;
+    stk[0].ensure((size_t)2 * P * h0 * h0);
+    stk[1].ensure((size_t)2 * h1 * P * h1);
+    for (int p = 0; p < P; p++) {
+      half_restack_kernel<<<gsz(2LL * h0 * h0), 256, 0, s>>>(stk[0].ptr, factors[p][0], coefs[p], p, P, nin[0], 0);
+      half_restack_kernel<<<gsz(2LL * h1 * h1), 256, 0, s>>>(stk[1].ptr, factors[p][1], 1.0, p, P, nin[1], 1);
+      count_launch(2);
+    }
+    check_launch("KronSum::build (parity)");
+    return;
+  }
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
   const int first = rev ? d - 1 : 0;
   mid_thin = (d == 3 && nout[1] == 1 && nin[1] > 1 && P <= 8 && !getenv("GPFVM_NO_MIDTHIN"));
@@ -251,6 +354,7 @@ int64_t KronSum::workspace_per_rhs() const {
 
 double KronSum::flops_per_rhs() const {
   if (P == 0) return 0.0;
+  if (par) return order_flops(d, P, nin, nout, false) / 2.0;
   if (mid_thin)
     return 2.0 * P * ((double)nin[0] * nin[1] * nin[2] + (double)nout[0] * nin[0] * nin[2] +
                       (double)nout[0] * nout[2] * nin[2]);
@@ -298,6 +402,38 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     return;
   }
   const int l = d - 1;
+  if (par) {
+    // X -> parity classes (w1), stage 0 over the time classes, stage 1 over the
+    // space classes, classes -> Y (+ low-rank term, beta)
+    const int h0 = nin[0] / 2, h1 = nin[1] / 2;
+    const int64_t cls = (int64_t)h0 * h1, zc = (int64_t)P * cls;
+    parity_fwd2_kernel<<<(unsigned)std::min<int64_t>((R * cls + 255) / 256, 148 * 16), 256, 0, s>>>(x, ldx, w1, R,
+                                                                                                   nin[0], nin[1]);
+    count_launch();
+    Gemm g0, g1;
+    // Z[a][(r,b)][(j0,p)][k1] = sum_k0 H0_a[(j0,p)][k0] Xt[a][(r,b)][k0][k1]
+    g0.M = P * h0; g0.N = h1; g0.K = h0;
+    g0.A = stk[0].ptr; g0.a_rs = h0; g0.a_cs = 1; g0.a_b1 = 0; g0.a_b2 = (int64_t)P * h0 * h0;
+    g0.B = w1; g0.b_rs = h1; g0.b_cs = 1; g0.b_b1 = cls; g0.b_b2 = 2LL * R * cls;
+    g0.C = w0; g0.c_rs = h1; g0.c_cs = 1; g0.c_b1 = zc; g0.c_b2 = 2LL * R * zc;
+    g0.batch1 = 2 * R; g0.batch2 = 2;
+    run_gemm(g0, s);
+    // Yt[(a,r)][b][j0][j1] = sum_(p,k1) Z[(a,r)][b][j0][(p,k1)] H1_b[j1][(p,k1)]
+    g1.M = h0; g1.N = h1; g1.K = P * h1;
+    g1.A = w0; g1.a_rs = (int64_t)P * h1; g1.a_cs = 1; g1.a_b1 = 2 * zc; g1.a_b2 = zc;
+    g1.B = stk[1].ptr; g1.b_rs = 1; g1.b_cs = (int64_t)P * h1; g1.b_b1 = 0; g1.b_b2 = (int64_t)h1 * P * h1;
+    g1.C = w1; g1.c_rs = h1; g1.c_cs = 1; g1.c_b1 = 2 * cls; g1.c_b2 = cls;
+    g1.batch1 = 2 * R; g1.batch2 = 2;
+    run_gemm(g1, s);
+    const bool lr = extra && extra->K2 > 0;
+    parity_inv2_kernel<<<(unsigned)std::min<int64_t>((R * cls + 255) / 256, 148 * 16), 256, 0, s>>>(
+        w1, y, ldy, R, nin[0], nin[1], sg[0], sg[1], beta, lr ? extra->A2 : nullptr, lr ? extra->a2_rs : 0,
+        lr ? extra->a2_b1 : 0, lr ? extra->B2 : nullptr, lr ? extra->b2_rs : 0, lr ? extra->b2_b1 : 0,
+        lr ? extra->K2 : 0);
+    count_launch();
+    check_launch("KronSum::apply (parity)");
+    return;
+  }
   if (mid_thin) {
     // A: R[r][a][p][k2] = sum_k1 f_p[k1] X_r[a][k1][k2]   (few-row GEMM over row-major slices)
     const int64_t rsz = (int64_t)nin[0] * P * nin[2], zsz = (int64_t)nout[0] * P * nin[2];

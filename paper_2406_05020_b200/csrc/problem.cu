@@ -1,5 +1,6 @@
 // C ABI: handle lifetime, factor assembly (§8 row 1) and the Kronecker Gram
 // matvec (§8 row 2).  See include/gpfvm.h for the contract and DESIGN.md §4.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -69,6 +70,18 @@ static void copy_sites(Sites& dst, const gpfvm_sites1d& src, int q_max_order_che
   }
 }
 
+// Even-length site list invariant under the reflection x -> c - x about its
+// centre (site i <-> site n-1-i), to 1e-14 of its extent.
+static bool mirror_symmetric(const Sites& S) {
+  if (S.n < 2 || S.n % 2) return false;
+  const int n = S.n;
+  const double c = S.lo[0] + S.hi[n - 1];
+  const double tol = 1e-14 * (std::fabs(S.lo[0]) + std::fabs(S.hi[n - 1]) + (S.hi[n - 1] - S.lo[0]));
+  for (int i = 0; i < n; i++)
+    if (!(std::fabs(S.lo[i] + S.hi[n - 1 - i] - c) <= tol)) return false;
+  return true;
+}
+
 int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr) {
   FactorKey key{out, dim, bl, ml, br, mr};
   auto it = p->factor_index.find(key);
@@ -76,6 +89,10 @@ int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int m
   Factor f;
   f.rows = p->blocks[bl].sites[dim].n;
   f.cols = p->blocks[br].sites[dim].n;
+  // a stationary kernel k(x - y) on one mirror-symmetric site list: the
+  // reflection maps cell i to n-1-i and each derivative flips sign, so
+  // F[n-1-i][n-1-j] = (-1)^(ml + mr) F[i][j]  (KronSum parity split)
+  if (bl == br && mirror_symmetric(p->blocks[bl].sites[dim])) f.psign = ((ml + mr) & 1) ? -1 : 1;
   p->factors.push_back(std::move(f));
   int id = (int)p->factors.size() - 1;
   p->factor_index[key] = id;
@@ -223,14 +240,20 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
     for (auto& op : p->plan->pairs) {
       std::vector<double> coefs;
       std::vector<std::vector<const double*>> fs;
+      std::vector<std::vector<int>> sgn;
       for (const auto& t : p->terms) {
         if (t.I != op.I || t.J != op.J) continue;
         coefs.push_back(t.coef);
         std::vector<const double*> f;
-        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        std::vector<int> sv;
+        for (int i = 0; i < p->ndim; i++) {
+          f.push_back(p->factors[t.fid[i]].data.ptr);
+          sv.push_back(op.I == op.J ? p->factors[t.fid[i]].psign : 0);
+        }
         fs.push_back(f);
+        sgn.push_back(sv);
       }
-      op.ks.build(p->ndim, p->blocks[op.J].shape, p->blocks[op.I].shape, coefs, fs, s);
+      op.ks.build(p->ndim, p->blocks[op.J].shape, p->blocks[op.I].shape, coefs, fs, s, &sgn);
     }
     return;
   }
@@ -241,18 +264,24 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
     for (int J = 0; J < nb; J++) {
       std::vector<double> coefs;
       std::vector<std::vector<const double*>> fs;
+      std::vector<std::vector<int>> sgn;
       for (const auto& t : p->terms) {
         if (t.I != I || t.J != J) continue;
         coefs.push_back(t.coef);
         std::vector<const double*> f;
-        for (int i = 0; i < p->ndim; i++) f.push_back(p->factors[t.fid[i]].data.ptr);
+        std::vector<int> sv;
+        for (int i = 0; i < p->ndim; i++) {
+          f.push_back(p->factors[t.fid[i]].data.ptr);
+          sv.push_back(I == J ? p->factors[t.fid[i]].psign : 0);
+        }
         fs.push_back(f);
+        sgn.push_back(sv);
       }
       if (coefs.empty()) continue;
       PairOp op;
       op.I = I;
       op.J = J;
-      op.ks.build(p->ndim, p->blocks[J].shape, p->blocks[I].shape, coefs, fs, s);
+      op.ks.build(p->ndim, p->blocks[J].shape, p->blocks[I].shape, coefs, fs, s, &sgn);
       plan->flops_per_rhs += op.ks.flops_per_rhs();
       plan->by_out[I].push_back((int)plan->pairs.size());
       plan->pairs.push_back(std::move(op));

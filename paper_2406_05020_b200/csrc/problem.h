@@ -23,6 +23,9 @@ using FactorKey = std::tuple<int, int, int, int, int, int>;
 
 struct Factor {
   int rows = 0, cols = 0;
+  // reflection parity of a square factor on a mirror-symmetric site list:
+  // F[n-1-i][n-1-j] = psign * F[i][j] (+1 centrosymmetric, -1 skew; 0: none)
+  int psign = 0;
   DevBuf data;  // row-major rows x cols
 };
 
@@ -51,8 +54,19 @@ struct KronSum {
   // 3D with a single output site in the last dimension (faces x = const of a
   // (t, y, x) layout): point functional first, then dimension 1, then time
   bool last_thin = false;
+  // reflection-parity split (d = 2): every factor of dimension
+  // i is centrosymmetric (sg[i] = 0) or skew-centrosymmetric (sg[i] = 1) on an
+  // even-length mirror-symmetric site list.  X is transformed to its even/odd
+  // parts per dimension (u = x_k + x_{n-1-k}, v = x_k - x_{n-1-k}), each factor
+  // splits into two half-size blocks E = F_top-left + F_top-right J and
+  // O = F_top-left - F_top-right J, and the Kronecker sum runs on the four
+  // parity classes as two-level batched GEMMs: half the flops of every stage
+  bool par = false;
+  int sg[GPFVM_MAX_DIMS] = {0, 0, 0, 0};
+  // signs (optional): per term, per dimension the factor's psign (0 = none)
   void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
-             const std::vector<std::vector<const double*>>& factors, cudaStream_t s);
+             const std::vector<std::vector<const double*>>& factors, cudaStream_t s,
+             const std::vector<std::vector<int>>* signs = nullptr);
   int64_t workspace_per_rhs() const;
   double flops_per_rhs() const;
   // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
