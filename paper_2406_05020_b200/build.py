@@ -5,7 +5,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["pool.cu", "assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "gemm_tma.cu", "shard.cu"]
+SOURCES = ["pool.cu", "assemble.cu", "gemm.cu", "kron.cu", "lowrank.cu", "funcpass.cu", "bjfd.cu", "linalg.cu", "vecops.cu", "problem.cu", "solve.cu", "predict.cu", "extras.cu", "gemm_tma.cu", "shard.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",
          "-Xcompiler", "-fPIC"]
 

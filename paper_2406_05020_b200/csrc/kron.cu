@@ -136,6 +136,60 @@ __global__ void parity_inv2_kernel(const double* __restrict__ yt, double* __rest
   }
 }
 
+// Vectorised variant (h1 even, 16-byte aligned rows): one thread per column
+// pair (j, j+1) of one half row; grid (column chunks, h0, R), no integer
+// division.  The mirrored columns n1-1-j, n1-2-j are one reversed double2.
+__global__ void __launch_bounds__(128)
+    parity_inv2v_kernel(const double* __restrict__ yt, double* __restrict__ y, int64_t ldy, int R, int n0, int n1,
+                        int sg0, int sg1, double beta, const double* __restrict__ U, int64_t u_rs, int64_t u_b1,
+                        const double* __restrict__ V, int64_t v_rs, int64_t v_b1, int rk) {
+  const int h0 = n0 >> 1, h1 = n1 >> 1;
+  const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x), i = blockIdx.y, r = blockIdx.z;
+  if (j >= h1) return;
+  const int64_t cls = (int64_t)h0 * h1, ij = (int64_t)i * h1 + j;
+  const double2 Y00 = *reinterpret_cast<const double2*>(yt + (((int64_t)(0 ^ sg0) * R + r) * 2 + (0 ^ sg1)) * cls + ij);
+  const double2 Y01 = *reinterpret_cast<const double2*>(yt + (((int64_t)(0 ^ sg0) * R + r) * 2 + (1 ^ sg1)) * cls + ij);
+  const double2 Y10 = *reinterpret_cast<const double2*>(yt + (((int64_t)(1 ^ sg0) * R + r) * 2 + (0 ^ sg1)) * cls + ij);
+  const double2 Y11 = *reinterpret_cast<const double2*>(yt + (((int64_t)(1 ^ sg0) * R + r) * 2 + (1 ^ sg1)) * cls + ij);
+  const int i1 = n0 - 1 - i, j1 = n1 - 2 - j;  // columns j1, j1 + 1 mirror j + 1, j
+  // o[row half][col half][column of the pair]
+  double oa[2] = {0.25 * ((Y00.x + Y01.x) + (Y10.x + Y11.x)), 0.25 * ((Y00.y + Y01.y) + (Y10.y + Y11.y))};  // (i, j..)
+  double ob[2] = {0.25 * ((Y00.x - Y01.x) + (Y10.x - Y11.x)), 0.25 * ((Y00.y - Y01.y) + (Y10.y - Y11.y))};  // (i, mirror)
+  double oc[2] = {0.25 * ((Y00.x + Y01.x) - (Y10.x + Y11.x)), 0.25 * ((Y00.y + Y01.y) - (Y10.y + Y11.y))};  // (i1, j..)
+  double od[2] = {0.25 * ((Y00.x - Y01.x) - (Y10.x - Y11.x)), 0.25 * ((Y00.y - Y01.y) - (Y10.y - Y11.y))};  // (i1, mirror)
+  if (rk > 0) {
+    const double* u0 = U + r * u_b1 + (int64_t)i * u_rs;
+    const double* u1 = U + r * u_b1 + (int64_t)i1 * u_rs;
+    const double* Vr = V + r * v_b1;
+    const double* wa0 = Vr + (int64_t)j * v_rs;
+    const double* wa1 = Vr + (int64_t)(j + 1) * v_rs;
+    const double* wb0 = Vr + (int64_t)(n1 - 1 - j) * v_rs;
+    const double* wb1 = Vr + (int64_t)(n1 - 2 - j) * v_rs;
+    for (int k = 0; k < rk; k++) {
+      const double a = u0[k], b = u1[k], p0 = wa0[k], p1 = wa1[k], q0 = wb0[k], q1 = wb1[k];
+      oa[0] = fma(a, p0, oa[0]); oa[1] = fma(a, p1, oa[1]);
+      ob[0] = fma(a, q0, ob[0]); ob[1] = fma(a, q1, ob[1]);
+      oc[0] = fma(b, p0, oc[0]); oc[1] = fma(b, p1, oc[1]);
+      od[0] = fma(b, q0, od[0]); od[1] = fma(b, q1, od[1]);
+    }
+  }
+  double* yr = y + r * ldy;
+  double2* pa = reinterpret_cast<double2*>(yr + (int64_t)i * n1 + j);
+  double2* pb = reinterpret_cast<double2*>(yr + (int64_t)i * n1 + j1);
+  double2* pc = reinterpret_cast<double2*>(yr + (int64_t)i1 * n1 + j);
+  double2* pd = reinterpret_cast<double2*>(yr + (int64_t)i1 * n1 + j1);
+  double2 va = make_double2(oa[0], oa[1]), vb = make_double2(ob[1], ob[0]);
+  double2 vc = make_double2(oc[0], oc[1]), vd = make_double2(od[1], od[0]);
+  if (beta != 0.0) {
+    const double2 a = *pa, b = *pb, c = *pc, d = *pd;
+    va.x = fma(beta, a.x, va.x); va.y = fma(beta, a.y, va.y);
+    vb.x = fma(beta, b.x, vb.x); vb.y = fma(beta, b.y, vb.y);
+    vc.x = fma(beta, c.x, vc.x); vc.y = fma(beta, c.y, vc.y);
+    vd.x = fma(beta, d.x, vd.x); vd.y = fma(beta, d.y, vd.y);
+  }
+  *pa = va; *pb = vb; *pc = vc; *pd = vd;
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -368,10 +422,14 @@ double KronSum::flops_per_rhs() const {
 }
 
 void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-                    cudaStream_t s, const Gemm* extra) const {
+                    cudaStream_t s, const Gemm* extra, cudaEvent_t extra_ready, const double* stage0) const {
+  if (extra_ready && !par) {  // only the parity path defers the wait to the kernel that reads the extra term
+    GPFVM_CUDA(cudaStreamWaitEvent(s, extra_ready, 0));
+    extra_ready = nullptr;
+  }
   if (extra && extra->K2 > 0 && !(d == 2 && !rev && P > 0)) {
     // not fusable here: the Kronecker sum, then the low-rank term as its own GEMM
-    apply(x, ldx, y, ldy, R, beta, w0, w1, s, nullptr);
+    apply(x, ldx, y, ldy, R, beta, w0, w1, s, nullptr, nullptr, stage0);
     Gemm e;
     e.M = d == 2 ? nout[0] : 1; e.N = nout[d - 1];
     for (int k = 1; k < d - 1; k++) e.M *= nout[k];
@@ -426,10 +484,21 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     g1.batch1 = 2 * R; g1.batch2 = 2;
     run_gemm(g1, s);
     const bool lr = extra && extra->K2 > 0;
-    parity_inv2_kernel<<<(unsigned)std::min<int64_t>((R * cls + 255) / 256, 148 * 16), 256, 0, s>>>(
-        w1, y, ldy, R, nin[0], nin[1], sg[0], sg[1], beta, lr ? extra->A2 : nullptr, lr ? extra->a2_rs : 0,
-        lr ? extra->a2_b1 : 0, lr ? extra->B2 : nullptr, lr ? extra->b2_rs : 0, lr ? extra->b2_b1 : 0,
-        lr ? extra->K2 : 0);
+    if (extra_ready) GPFVM_CUDA(cudaStreamWaitEvent(s, extra_ready, 0));  // U, V prepared on a side stream
+    const double* Ue = lr ? extra->A2 : nullptr;
+    const double* Ve = lr ? extra->B2 : nullptr;
+    const bool vec = (h1 % 2 == 0) && ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(w1)) & 15) == 0 &&
+                     (ldy % 2 == 0) && h0 <= 65535 && R <= 65535;
+    if (vec) {
+      const dim3 grid((unsigned)((h1 / 2 + 127) / 128), (unsigned)h0, (unsigned)R);
+      parity_inv2v_kernel<<<grid, 128, 0, s>>>(w1, y, ldy, R, nin[0], nin[1], sg[0], sg[1], beta, Ue, lr ? extra->a2_rs : 0,
+                                               lr ? extra->a2_b1 : 0, Ve, lr ? extra->b2_rs : 0, lr ? extra->b2_b1 : 0,
+                                               lr ? extra->K2 : 0);
+    } else {
+      parity_inv2_kernel<<<(unsigned)std::min<int64_t>((R * cls + 255) / 256, 148 * 16), 256, 0, s>>>(
+          w1, y, ldy, R, nin[0], nin[1], sg[0], sg[1], beta, Ue, lr ? extra->a2_rs : 0, lr ? extra->a2_b1 : 0, Ve,
+          lr ? extra->b2_rs : 0, lr ? extra->b2_b1 : 0, lr ? extra->K2 : 0);
+    }
     count_launch();
     check_launch("KronSum::apply (parity)");
     return;
@@ -532,7 +601,11 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
       g1.A2 = extra->A2; g1.a2_rs = extra->a2_rs; g1.a2_b1 = extra->a2_b1;
       g1.B2 = extra->B2; g1.b2_rs = extra->b2_rs; g1.b2_b1 = extra->b2_b1;
     }
-    run_gemm(g0, s);
+    if (stage0) {
+      (rev ? g1.B : g1.A) = stage0;
+    } else {
+      run_gemm(g0, s);
+    }
     run_gemm(g1, s);
     return;
   }

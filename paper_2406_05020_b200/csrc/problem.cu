@@ -224,6 +224,13 @@ MatvecPlan::~MatvecPlan() {
   for (auto st : branch) cudaStreamDestroy(st);
   if (cap) cudaStreamDestroy(cap);
   for (auto e : ev) cudaEventDestroy(e);
+  for (auto& ff : fused)
+    if (ff.ev) cudaEventDestroy(ff.ev);
+  for (auto& lr : lowrank) {
+    if (lr.side) cudaStreamDestroy(lr.side);
+    if (lr.ev_fork) cudaEventDestroy(lr.ev_fork);
+    if (lr.ev_ready) cudaEventDestroy(lr.ev_ready);
+  }
 }
 
 void MatvecPlan::release_graphs() {
@@ -289,6 +296,7 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
   plan->w0.resize(nb);
   plan->w1.resize(nb);
   build_lowrank(p, *plan, s);
+  build_fused_func(p, *plan, s);
   // executed flops per right-hand side: plain pairs + low-rank / mode updates
   plan->flops_per_rhs = 0.0;
   for (const auto& op : plan->pairs)
@@ -307,9 +315,14 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
   p->plan = std::move(plan);
 }
 
+static int only_branch() {
+  static const int only = getenv("GPFVM_TIMING_ONLY_BRANCH") ? atoi(getenv("GPFVM_TIMING_ONLY_BRANCH")) : -1;
+  return only;
+}
+
 static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
   MatvecPlan& pl = *p->plan;
-  static const int only = getenv("GPFVM_TIMING_ONLY_BRANCH") ? atoi(getenv("GPFVM_TIMING_ONLY_BRANCH")) : -1;
+  const int only = only_branch();
   if (only >= 0 && I != only) return;  // timing experiments only: wrong results
   const BlockInt& B = p->blocks[I];
   // noise-free block: the first pair overwrites (beta = 0), saving one read-modify-write pass
@@ -323,9 +336,28 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
     if (pl.pairs[k].J == I && !pl.pairs[k].lowrank) diag = &pl.pairs[k];
   static const bool no_fuse = getenv("GPFVM_NO_LRFUSE") != nullptr;
   Gemm lr_extra;
+  cudaEvent_t lr_ready = nullptr;
   if (lr.rk > 0) {
     if (diag && !no_fuse) {
-      lr.prepare(x, ld, nrhs, pl.block_off.data(), s);
+      // parity-split Kronecker sum: U, V are read only by its last kernel, so
+      // they are prepared on a side stream beside the two mode products
+      static const bool no_fork = getenv("GPFVM_NO_LRFORK") != nullptr;
+      if (diag->ks.par && !no_fork) {
+        if (!lr.side) {
+          int lo = 0, hi = 0;
+          GPFVM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+          GPFVM_CUDA(cudaStreamCreateWithPriority(&lr.side, cudaStreamNonBlocking, lo));
+          GPFVM_CUDA(cudaEventCreateWithFlags(&lr.ev_fork, cudaEventDisableTiming));
+          GPFVM_CUDA(cudaEventCreateWithFlags(&lr.ev_ready, cudaEventDisableTiming));
+        }
+        GPFVM_CUDA(cudaEventRecord(lr.ev_fork, s));
+        GPFVM_CUDA(cudaStreamWaitEvent(lr.side, lr.ev_fork, 0));
+        lr.prepare(x, ld, nrhs, pl.block_off.data(), lr.side);
+        GPFVM_CUDA(cudaEventRecord(lr.ev_ready, lr.side));
+        lr_ready = lr.ev_ready;
+      } else {
+        lr.prepare(x, ld, nrhs, pl.block_off.data(), s);
+      }
       lr.as_extra(lr_extra, nrhs);
     } else {
       lr.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), s);
@@ -340,8 +372,15 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
   for (int k : pl.by_out[I]) {
     const PairOp& op = pl.pairs[k];
     if (op.lowrank) continue;
+    const double* stage0 = nullptr;
+    if (pl.fused_on && pl.fused_of[k] >= 0) {
+      const FusedFunc& ff = pl.fused[pl.fused_of[k]];
+      GPFVM_CUDA(cudaStreamWaitEvent(s, ff.ev, 0));
+      stage0 = ff.stage0_of(k, nrhs);
+    }
     op.ks.apply(x + p->blocks[op.J].offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr,
-                pl.w1[I].ptr, s, (&op == diag && lr_extra.K2 > 0) ? &lr_extra : nullptr);
+                pl.w1[I].ptr, s, (&op == diag && lr_extra.K2 > 0) ? &lr_extra : nullptr,
+                (&op == diag && lr_extra.K2 > 0) ? lr_ready : nullptr, stage0);
     overwrite = false;
   }
 }
@@ -365,6 +404,14 @@ static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
       pl.w0[I].ensure(n);
       pl.w1[I].ensure(n);
     }
+    if (I == 0)
+      for (auto& ff : pl.fused) {
+        const size_t nz = (size_t)ff.zper * nrhs, nc = (size_t)nrhs * ff.tiles() * 4 * ff.n1;
+        if (ff.zbuf.n < nz || ff.colpart.n < nc) {
+          pl.release_graphs();
+          ff.ensure(nrhs);
+        }
+      }
     LowRank& lr = pl.lowrank[I];
     if (lr.rk > 0) {
       int pmax = 1;
@@ -422,10 +469,26 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
   }
   // one branch per output block on its own stream, forked from and joined
   // into `s` (direct launch) or the capture stream (graph)
+  // the fused functional passes need 16-byte aligned rows of x
+  pl.fused_on = !pl.fused.empty() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ld & 1) == 0 && only_branch() < 0 &&
+                (int64_t)nrhs * pl.fused[0].tiles() >= 64;  // few vectors: too few CTAs for one pass to pay
   auto run_branches = [&](cudaStream_t origin) {
     GPFVM_CUDA(cudaEventRecord(pl.ev[nb], origin));
+    std::vector<char> waited(nb, 0);
+    if (pl.fused_on)
+      for (auto& ff : pl.fused) {
+        // first on the input block's own branch stream (measured: 1.024 ms against
+        // 1.052 ms on a consumer's stream beside the parity transform); the
+        // consumers wait on ff.ev
+        const int sb = ff.J;
+        cudaStream_t fs = pl.branch[sb];
+        if (!waited[sb]) GPFVM_CUDA(cudaStreamWaitEvent(fs, pl.ev[nb], 0));
+        waited[sb] = 1;
+        ff.run(x + p->blocks[ff.J].offset, ld, nrhs, fs);
+        GPFVM_CUDA(cudaEventRecord(ff.ev, fs));
+      }
     for (int I = 0; I < nb; I++) {
-      GPFVM_CUDA(cudaStreamWaitEvent(pl.branch[I], pl.ev[nb], 0));
+      if (!waited[I]) GPFVM_CUDA(cudaStreamWaitEvent(pl.branch[I], pl.ev[nb], 0));
       matvec_branch(p, I, x, y, nrhs, ld, pl.branch[I]);
       GPFVM_CUDA(cudaEventRecord(pl.ev[I], pl.branch[I]));
       GPFVM_CUDA(cudaStreamWaitEvent(origin, pl.ev[I], 0));

@@ -72,8 +72,13 @@ struct KronSum {
   // y = beta*y + sum_p (x)F^p x  for R vectors; w0/w1: R*workspace_per_rhs() doubles each
   // extra: optional low-rank term (Gemm::K2 fields) added to the result, fused
   // into the last contraction where its layout allows (2D forward order)
+  // extra_ready: event after which the extra term's operands are valid (they
+  // may be prepared on another stream while the contractions run)
+  // stage0 (d = 2, plain path): the result of the first contraction, already
+  // computed elsewhere (FusedFunc) in the layout this plan's stage 0 writes
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-             cudaStream_t s, const Gemm* extra = nullptr) const;
+             cudaStream_t s, const Gemm* extra = nullptr, cudaEvent_t extra_ready = nullptr,
+             const double* stage0 = nullptr) const;
 };
 
 // Per-block fast-diagonalisation (bjfd.cu)
@@ -148,6 +153,9 @@ struct LowRank {
   std::vector<Part> parts;
   DevBuf U, V, T;  // U [R][n0][rkp], V (transposed) [R][n1][rkp], scratch T
   int R = 0;
+  // side stream on which prepare() runs beside the block's own Kronecker sum
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_ready = nullptr;
   int rkp() const { return (rk + 1) & ~1; }  // even row stride (16-byte TMA strides)
   // U and V of y += U V^T for the current input (the coupling GEMMs)
   void prepare(const double* x, int64_t ldx, int Rn, const int64_t* block_off, cudaStream_t s);
@@ -185,6 +193,26 @@ struct ModeUpdate {
              double* w0, double* w1, cudaStream_t s) const;
 };
 
+// One read of a 2D input block J for every thin pair (I, J) (funcpass.cu): the
+// first contraction of each such pair (a time-point or space-point functional
+// of the whole block) evaluated together; the pairs' KronSums then start at
+// their second contraction (KronSum::apply `stage0`).
+struct FusedFunc {
+  struct Out {
+    int pair, type, P, first;  // type 0: column sums (IC-like), 1: row sums (BC-like); first slot of its P functionals
+    int64_t off;               // per-RHS offset of the pair's stage-0 result inside zbuf
+  };
+  int J = 0, n0 = 0, n1 = 0, NC = 0, NR = 0;
+  int64_t zper = 0;            // stage-0 doubles per RHS over all pairs
+  std::vector<Out> outs;
+  DevBuf wc, wr, zbuf, colpart;
+  cudaEvent_t ev = nullptr;
+  int tiles() const;
+  void ensure(int R);
+  void run(const double* xJ, int64_t ldx, int R, cudaStream_t s) const;
+  const double* stage0_of(int pair, int R) const;
+};
+
 // Matvec plan: one KronSum per nonzero block pair, grouped by output block
 // (graph branches), with CUDA-graph replay cached per (x, y, nrhs, ld).
 struct MatvecPlan {
@@ -192,6 +220,9 @@ struct MatvecPlan {
   std::vector<std::vector<int>> by_out;
   std::vector<LowRank> lowrank;  // per output block (rk = 0: unused)
   std::vector<std::vector<ModeUpdate>> modes;  // per output block (d >= 3)
+  std::vector<FusedFunc> fused;  // per 2D input block with >= 2 thin pairs
+  std::vector<int> fused_of;     // per pair: index into fused or -1
+  bool fused_on = false;         // this launch uses the fused pass (alignment checked per call)
   std::vector<int64_t> block_off;
   std::vector<DevBuf> w0, w1;  // per output-block branch
   std::vector<cudaStream_t> branch;
@@ -247,6 +278,7 @@ void apply_terms(gpfvm_problem* p, const std::vector<Factor>& factors, const std
 void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s);
 void build_plan(gpfvm_problem* p, cudaStream_t s);
 void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s);
+void build_fused_func(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s);
 double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape);
 int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr);
 
