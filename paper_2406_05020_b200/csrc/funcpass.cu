@@ -225,23 +225,32 @@ void build_fused_func(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s) {
     ff.wr.ensure((size_t)4 * n1);
     fill(ff.wc.ptr, 0.0, 4 * (int64_t)n0, s);
     fill(ff.wr.ptr, 0.0, 4 * (int64_t)n1, s);
-    for (const auto& o : ff.outs) {
-      const KronSum& ks = pl.pairs[o.pair].ks;
-      // column type (forward order): stk[0] = c_p F0^p rows (P x n0); row type
-      // (reverse order): stk[1] = c_p F1^p rows (P x n1)
-      if (o.type == 0)
-        GPFVM_CUDA(cudaMemcpyAsync(ff.wc.ptr + (int64_t)o.first * n0, ks.stk[0].ptr, sizeof(double) * o.P * n0,
-                                   cudaMemcpyDeviceToDevice, s));
-      else
-        GPFVM_CUDA(cudaMemcpyAsync(ff.wr.ptr + (int64_t)o.first * n1, ks.stk[1].ptr, sizeof(double) * o.P * n1,
-                                   cudaMemcpyDeviceToDevice, s));
-    }
     GPFVM_CUDA(cudaEventCreateWithFlags(&ff.ev, cudaEventDisableTiming));
     pl.fused.push_back(std::move(ff));
   }
   pl.fused_of.assign(pl.pairs.size(), -1);
   for (size_t f = 0; f < pl.fused.size(); f++)
     for (const auto& o : pl.fused[f].outs) pl.fused_of[o.pair] = (int)f;
+  refresh_fused_func(pl, s);
+}
+
+// The functional weights are the pairs' stage-0 factors (coefficients folded
+// in): copied again whenever the factors are re-assembled.
+void refresh_fused_func(MatvecPlan& pl, cudaStream_t s) {
+  for (auto& ff : pl.fused)
+    for (const auto& o : ff.outs) {
+      const KronSum& ks = pl.pairs[o.pair].ks;
+      // the plan of a thin pair is fixed by its shapes (re-assembly keeps it)
+      GPFVM_CHECK(ks.P == o.P && (o.type == 0 ? !ks.rev : ks.rev), GPFVM_ERR_STATE, "fused functional plan changed");
+      // column type (forward order): stk[0] = c_p F0^p rows (P x n0); row type
+      // (reverse order): stk[1] = c_p F1^p rows (P x n1)
+      if (o.type == 0)
+        GPFVM_CUDA(cudaMemcpyAsync(ff.wc.ptr + (int64_t)o.first * ff.n0, ks.stk[0].ptr, sizeof(double) * o.P * ff.n0,
+                                   cudaMemcpyDeviceToDevice, s));
+      else
+        GPFVM_CUDA(cudaMemcpyAsync(ff.wr.ptr + (int64_t)o.first * ff.n1, ks.stk[1].ptr, sizeof(double) * o.P * ff.n1,
+                                   cudaMemcpyDeviceToDevice, s));
+    }
 }
 
 }  // namespace gpfvm

@@ -105,7 +105,14 @@ template <int BM, int BN, int STAGES>
 struct TmaSmem {
   static constexpr int A_BYTES = BM * 128;  // [BM][16] doubles
   static constexpr int B_BYTES = BN * 128;  // [BN][16] or [BN/16][16][16]
-  static constexpr size_t bytes = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
+  static constexpr size_t raw_bytes = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
+  // At least 117 KB (more than half of the SM's 227 KB): at most ONE CTA of
+  // any variant of this kernel is resident per SM.  CTAs of two different
+  // launches of the kernel sharing an SM (concurrent streams / graph branches,
+  // small tiles with 2-3 CTAs per SM) produced partially wrong tiles,
+  // nondeterministically (found on config 4 / config 2; never
+  // with one launch at a time, never with one CTA per SM).
+  static constexpr size_t bytes = raw_bytes > 117 * 1024 ? raw_bytes : 117 * 1024;
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool BROW, int MINB>
@@ -251,16 +258,25 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, MINB)
     for (int i = 0; i < TM; i++) {
       const int row = m0 + wm0 + i * 8 + g8;
       if (row >= g.M) continue;
+      double* crow = C + (int64_t)row * g.c_rs + n0 + wn0 + 2 * q;
+      const int col0 = n0 + wn0 + 2 * q;
+      // beta != 0: all the row's old values first (TN independent 16-byte loads
+      // in flight per lane instead of a load -> fma -> store chain per pair)
+      double2 old[TN];
+      if (g.beta != 0.0) {
+#pragma unroll
+        for (int j = 0; j < TN; j++)
+          old[j] = (col0 + j * 8 + 1 < g.N) ? *reinterpret_cast<const double2*>(crow + j * 8) : make_double2(0.0, 0.0);
+      }
 #pragma unroll
       for (int j = 0; j < TN; j++) {
-        const int col = n0 + wn0 + j * 8 + 2 * q;
-        double* cp = C + (int64_t)row * g.c_rs + col;
+        const int col = col0 + j * 8;
+        double* cp = crow + j * 8;
         double v0 = g.alpha * acc[i][j][0], v1 = g.alpha * acc[i][j][1];
         if (col + 1 < g.N) {
           if (g.beta != 0.0) {
-            const double2 o = *reinterpret_cast<const double2*>(cp);
-            v0 += g.beta * o.x;
-            v1 += g.beta * o.y;
+            v0 += g.beta * old[j].x;
+            v1 += g.beta * old[j].y;
           }
           *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
         } else if (col < g.N) {
@@ -340,10 +356,11 @@ template <int BM_, int BN_, int WM_, int WN_, int ST_, int MINB_>
 struct TileCfg {
   static constexpr int BM = BM_, BN = BN_, WMr = WM_, WNr = WN_, ST = ST_, MINB = MINB_;
 };
-using V0 = TileCfg<128, 64, 4, 2, 4, 2>;   // 32x32 warp tiles
-using V1 = TileCfg<64, 64, 2, 2, 4, 2>;    // small grids (6 stages gave wrong tiles in cold runs)
-using V2 = TileCfg<128, 64, 2, 2, 4, 2>;   // 64x32 warp tiles
-using V3 = TileCfg<128, 128, 2, 4, 4, 1>;  // 64x32 warp tiles, 8 consumer warps
+// every variant: 8 consumer warps, one CTA per SM (see TmaSmem::bytes)
+using V0 = TileCfg<128, 64, 4, 2, 6, 1>;   // 32x32 warp tiles
+using V1 = TileCfg<64, 64, 4, 2, 6, 1>;    // 16x32 warp tiles (small grids)
+using V2 = TileCfg<128, 64, 2, 2, 4, 1>;   // 64x32 warp tiles, 4 consumer warps
+using V3 = TileCfg<128, 128, 2, 4, 4, 1>;  // 64x32 warp tiles
 using V4 = TileCfg<128, 128, 4, 2, 4, 1>;  // 32x64 warp tiles
 using V5 = TileCfg<256, 64, 4, 2, 3, 1>;   // 64x32 warp tiles
 
@@ -418,22 +435,24 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
     default: break;
   }
   // Tile choice: estimated time = waves x tile work / relative DMMA efficiency
-  // of the tile shape (measured on the mode-product shapes, tools/gemm_bench:
-  // 128x128 with 32x64 warp tiles 1.0, 128x64 with 64x32 warp tiles 0.98,
-  // 64x64 0.85), waves = ceil(tiles / resident slots).
-  auto cost = [&](int bm, int bn, int per_sm, double eff) {
+  // of the tile shape (128x128 with 32x64 warp tiles 1.0, 128x64 with 32x32
+  // warp tiles 0.92, 64x64 with 16x32 warp tiles 0.8), waves = ceil(tiles / 148).
+  auto cost = [&](int bm, int bn, double eff) {
     const int64_t tiles = ((g.M + bm - 1) / bm) * (int64_t)((g.N + bn - 1) / bn) * batch;
-    const int64_t slots = 148LL * per_sm;
-    return (double)((tiles + slots - 1) / slots) * bm * bn * per_sm / eff;
+    return (double)((tiles + 147) / 148) * bm * bn / eff;
   };
-  // grids that cannot fill the machine even with 64x64 tiles go to the
-  // cp.async kernel's 32x32 tiles (more CTAs; these are the short IC/BC
-  // coupling GEMMs that run concurrently with the PDE branch)
-  static const int min_tiles = getenv("GPFVM_TMA_MIN_TILES") ? atoi(getenv("GPFVM_TMA_MIN_TILES")) : 148;
+  // Every eligible GEMM runs here, however small its grid.  Routing the small
+  // IC/BC coupling GEMMs to the cp.async kernel (more, smaller CTAs) was
+  // slightly faster on config 2 but made this kernel's results
+  // nondeterministically wrong when CTAs of the two kernels shared SMs on
+  // concurrent streams (config 4: 23 of 40 matvecs had wrong tiles; with every
+  // GEMM on this kernel 0 of 110).  GPFVM_TMA_MIN_TILES restores
+  // the threshold for experiments.
+  static const int min_tiles = getenv("GPFVM_TMA_MIN_TILES") ? atoi(getenv("GPFVM_TMA_MIN_TILES")) : 0;
   if (((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * batch < min_tiles) return false;
-  const double c4 = cost(128, 128, 1, 1.0), c2 = cost(128, 64, 2, 0.98), c1 = cost(64, 64, 2, 0.85);
-  if (c4 <= c2 && c4 <= c1) return run(V4{});
-  if (c2 <= c1) return run(V2{});
+  const double c4 = cost(128, 128, 1.0), c0 = cost(128, 64, 0.92), c1 = cost(64, 64, 0.8);
+  if (c4 <= c0 && c4 <= c1) return run(V4{});
+  if (c0 <= c1) return run(V0{});
   return run(V1{});
 }
 

@@ -190,6 +190,120 @@ __global__ void __launch_bounds__(128)
   *pa = va; *pb = vb; *pc = vc; *pd = vd;
 }
 
+// ---- 3D reflection-parity split (KronSum::par3) ------------------------------------
+// Half blocks of one factor, both classes back to back: dst[c][j][k] (h x h)
+//   = coef (F[j][k] + (-1)^c F[j][n-1-k]);  rows optionally interleaved over a
+// group of G factors (row (j, g) of a [c][(j, g)][k] stack).
+__global__ void half_block_kernel(double* dst, const double* __restrict__ F, double coef, int n, int g, int G) {
+  const int h = n / 2;
+  const int64_t tot = 2LL * h * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / ((int64_t)h * h));
+    const int j = (int)((e / h) % h), k = (int)(e % h);
+    const double a = F[(int64_t)j * n + k], b = F[(int64_t)j * n + (n - 1 - k)];
+    dst[(int64_t)c * G * h * h + ((int64_t)j * G + g) * h + k] = coef * (c ? a - b : a + b);
+  }
+}
+
+// x (n0 x n1 x n2) -> xt, same shape, index (class, half index) per dimension:
+// class 0 = x_k + x_{n-1-k}, class 1 = x_k - x_{n-1-k} (no scaling).
+// grid (ceil(h2 / 128), h1, h0 * Rc); one thread per (r, i, j, k), 8 in, 8 out.
+__global__ void __launch_bounds__(128)
+    parity_fwd3_kernel(const double* __restrict__ x, int64_t ldx, double* __restrict__ xt, int64_t ldt, int n0,
+                       int n1, int n2) {
+  const int h0 = n0 >> 1, h1 = n1 >> 1, h2 = n2 >> 1;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  const int i = blockIdx.z % h0, r = blockIdx.z / h0;
+  if (k >= h2) return;
+  const double* xr = x + (int64_t)r * ldx;
+  double v[8];
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    const int ii = (m & 4) ? n0 - 1 - i : i, jj = (m & 2) ? n1 - 1 - j : j, kk = (m & 1) ? n2 - 1 - k : k;
+    v[m] = xr[((int64_t)ii * n1 + jj) * n2 + kk];
+  }
+#pragma unroll
+  for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+    for (int m = 0; m < 8; m++)
+      if (!(m & bit)) {
+        const double a = v[m], b = v[m | bit];
+        v[m] = a + b;
+        v[m | bit] = a - b;
+      }
+  double* tr = xt + (int64_t)r * ldt;
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    const int ii = ((m & 4) ? h0 : 0) + i, jj = ((m & 2) ? h1 : 0) + j, kk = ((m & 1) ? h2 : 0) + k;
+    tr[((int64_t)ii * n1 + jj) * n2 + kk] = v[m];
+  }
+}
+
+// y = beta y + (1/8) inverse transform of yt + the mode-s updates of the block
+// (ModeTerms: couplings from IC planes and boundary faces), all in the one
+// pass that writes y.  Each thread owns the 8 mirror images of (i, j, k), so
+// every W value it loads serves two outputs.
+__global__ void __launch_bounds__(128)
+    parity_inv3_kernel(const double* __restrict__ yt, int64_t ldt, double* __restrict__ y, int64_t ldy, int n0, int n1,
+                       int n2, double beta, ModeTerms mt) {
+  const int h0 = n0 >> 1, h1 = n1 >> 1, h2 = n2 >> 1;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  const int i = blockIdx.z % h0, r = blockIdx.z / h0;
+  if (k >= h2) return;
+  const double* tr = yt + (int64_t)r * ldt;
+  double v[8];
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    const int ii = ((m & 4) ? h0 : 0) + i, jj = ((m & 2) ? h1 : 0) + j, kk = ((m & 1) ? h2 : 0) + k;
+    v[m] = tr[((int64_t)ii * n1 + jj) * n2 + kk];
+  }
+#pragma unroll
+  for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+    for (int m = 0; m < 8; m++)
+      if (!(m & bit)) {
+        const double a = v[m], b = v[m | bit];
+        v[m] = a + b;
+        v[m | bit] = a - b;
+      }
+#pragma unroll
+  for (int m = 0; m < 8; m++) v[m] *= 0.125;
+  const int I2[2] = {i, n0 - 1 - i}, J2[2] = {j, n1 - 1 - j}, K2[2] = {k, n2 - 1 - k};
+  for (int e = 0; e < mt.n; e++) {
+    const int P = mt.m[e].P, sd = mt.m[e].s;
+    const double* U = mt.m[e].U;
+    // a: index into U (the updated dimension); (b, c): the two indices of W
+    const int ia[2] = {sd == 0 ? I2[0] : (sd == 1 ? J2[0] : K2[0]), sd == 0 ? I2[1] : (sd == 1 ? J2[1] : K2[1])};
+    const int ib[2] = {sd == 0 ? J2[0] : I2[0], sd == 0 ? J2[1] : I2[1]};
+    const int ic[2] = {sd == 2 ? J2[0] : K2[0], sd == 2 ? J2[1] : K2[1]};
+    const int64_t nc = sd == 2 ? n1 : n2, AB = (sd == 0 ? (int64_t)n1 : (int64_t)n0) * nc;
+    const double* W = mt.m[e].W + (int64_t)r * P * AB;
+    for (int p = 0; p < P; p++) {
+      const double u0 = U[(int64_t)ia[0] * P + p], u1 = U[(int64_t)ia[1] * P + p];
+      const double* Wp = W + (int64_t)p * AB;
+      const double w00 = Wp[ib[0] * nc + ic[0]], w01 = Wp[ib[0] * nc + ic[1]];
+      const double w10 = Wp[ib[1] * nc + ic[0]], w11 = Wp[ib[1] * nc + ic[1]];
+      // output m = (mi, mj, mk) bits 4, 2, 1
+      if (sd == 0) {        // a = i, (b, c) = (j, k)
+        v[0] = fma(u0, w00, v[0]); v[1] = fma(u0, w01, v[1]); v[2] = fma(u0, w10, v[2]); v[3] = fma(u0, w11, v[3]);
+        v[4] = fma(u1, w00, v[4]); v[5] = fma(u1, w01, v[5]); v[6] = fma(u1, w10, v[6]); v[7] = fma(u1, w11, v[7]);
+      } else if (sd == 1) { // a = j, (b, c) = (i, k)
+        v[0] = fma(u0, w00, v[0]); v[1] = fma(u0, w01, v[1]); v[2] = fma(u1, w00, v[2]); v[3] = fma(u1, w01, v[3]);
+        v[4] = fma(u0, w10, v[4]); v[5] = fma(u0, w11, v[5]); v[6] = fma(u1, w10, v[6]); v[7] = fma(u1, w11, v[7]);
+      } else {              // a = k, (b, c) = (i, j)
+        v[0] = fma(u0, w00, v[0]); v[1] = fma(u1, w00, v[1]); v[2] = fma(u0, w01, v[2]); v[3] = fma(u1, w01, v[3]);
+        v[4] = fma(u0, w10, v[4]); v[5] = fma(u1, w10, v[5]); v[6] = fma(u0, w11, v[6]); v[7] = fma(u1, w11, v[7]);
+      }
+    }
+  }
+  double* yr = y + (int64_t)r * ldy;
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    double* yp = yr + ((int64_t)I2[m >> 2] * n1 + J2[(m >> 1) & 1]) * n2 + K2[m & 1];
+    *yp = (beta != 0.0) ? fma(beta, *yp, v[m]) : v[m];
+  }
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -270,6 +384,71 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
       count_launch(2);
     }
     check_launch("KronSum::build (parity)");
+    return;
+  }
+  // 3D reflection-parity split: every factor is centrosymmetric
+  // or skew on an even-length mirror-symmetric site list.  The transformed
+  // vector keeps its shape with index (class, half index) per dimension; a
+  // factor maps input class c to class c ^ skew through its half block H_c, so
+  // every contraction of the forward plan becomes a class-batched GEMM with
+  // half M and half K: half the flops of every stage.
+  // smallest half size worth splitting (read per build: tests lower it)
+  const int par3_minh = getenv("GPFVM_PAR3_MINH") ? atoi(getenv("GPFVM_PAR3_MINH")) : 32;
+  par3 = (d == 3) && !no_par;
+  for (int i = 0; i < d && par3; i++) {
+    par3 = nin[i] == nout[i] && nin[i] % 4 == 0 && nin[i] / 2 >= par3_minh;
+    for (int p = 0; p < P && par3; p++) par3 = signs[p][i] != 0;
+  }
+  if (par3) {
+    rev = mid_thin = last_thin = false;
+    const int h0 = nin[0] / 2, h1 = nin[1] / 2, h2 = nin[2] / 2;
+    // distinct dim-0 / dim-2 factors, centrosymmetric ones first
+    std::vector<const double*> d0, d2;
+    std::vector<int> s0, s2;
+    for (int pass = 0; pass < 2; pass++)
+      for (int p = 0; p < P; p++) {
+        if ((signs[p][0] < 0) == (pass == 1) && std::find(d0.begin(), d0.end(), factors[p][0]) == d0.end()) {
+          d0.push_back(factors[p][0]);
+          s0.push_back(pass);
+        }
+        if ((signs[p][2] < 0) == (pass == 1) && std::find(d2.begin(), d2.end(), factors[p][2]) == d2.end()) {
+          d2.push_back(factors[p][2]);
+          s2.push_back(pass);
+        }
+      }
+    Q0 = (int)d0.size();
+    Q2 = (int)d2.size();
+    Qs0 = (int)std::count(s0.begin(), s0.end(), 0);
+    Qs2 = (int)std::count(s2.begin(), s2.end(), 0);
+    u0.assign(P, 0);
+    u2.assign(P, 0);
+    sk1.assign(P, 0);
+    for (int p = 0; p < P; p++) {
+      u0[p] = (int)(std::find(d0.begin(), d0.end(), factors[p][0]) - d0.begin());
+      u2[p] = (int)(std::find(d2.begin(), d2.end(), factors[p][2]) - d2.begin());
+      sk1[p] = signs[p][1] < 0;
+    }
+    stk[0].ensure((size_t)2 * Q0 * h0 * h0);
+    stk[1].ensure((size_t)2 * P * h1 * h1);
+    stk[2].ensure((size_t)2 * Q2 * h2 * h2);
+    // stk[0]: group (centrosymmetric | skew) stacks [c][(j, qg)][k]
+    for (int q = 0; q < Q0; q++) {
+      const bool skew = q >= Qs0;
+      const int G = skew ? Q0 - Qs0 : Qs0, g = skew ? q - Qs0 : q;
+      half_block_kernel<<<gsz(2LL * h0 * h0), 256, 0, s>>>(stk[0].ptr + (skew ? (int64_t)2 * Qs0 * h0 * h0 : 0), d0[q], 1.0,
+                                                           nin[0], g, G);
+      count_launch();
+    }
+    for (int p = 0; p < P; p++) {
+      half_block_kernel<<<gsz(2LL * h1 * h1), 256, 0, s>>>(stk[1].ptr + (int64_t)p * 2 * h1 * h1, factors[p][1], coefs[p],
+                                                           nin[1], 0, 1);
+      count_launch();
+    }
+    for (int q = 0; q < Q2; q++) {
+      half_block_kernel<<<gsz(2LL * h2 * h2), 256, 0, s>>>(stk[2].ptr + (int64_t)q * 2 * h2 * h2, d2[q], 1.0, nin[2], 0, 1);
+      count_launch();
+    }
+    check_launch("KronSum::build (3D parity)");
     return;
   }
   rev = (d > 1) && order_flops(d, P, nin, nout, true) < order_flops(d, P, nin, nout, false);
@@ -392,6 +571,7 @@ void KronSum::build(int d_, const int* in_shape, const int* out_shape, const std
 
 int64_t KronSum::workspace_per_rhs() const {
   if (P == 0 || d == 1) return 0;
+  if (par3) return (int64_t)std::max(std::max(Q0, Q2), 1) * nin[0] * nin[1] * nin[2];
   if (mid_thin) return (int64_t)std::max(nin[0], nout[0]) * P * nin[2];
   if (last_thin) return (int64_t)nin[0] * P * std::max(nin[1], nout[1]);
   int64_t mx = 0;
@@ -409,6 +589,9 @@ int64_t KronSum::workspace_per_rhs() const {
 double KronSum::flops_per_rhs() const {
   if (P == 0) return 0.0;
   if (par) return order_flops(d, P, nin, nout, false) / 2.0;
+  if (par3)
+    return ((double)Q0 * nout[0] * nin[0] * nin[1] * nin[2] + (double)P * nout[0] * nout[1] * nin[1] * nin[2] +
+            (double)Q2 * nout[0] * nout[1] * nout[2] * nin[2]);
   if (mid_thin)
     return 2.0 * P * ((double)nin[0] * nin[1] * nin[2] + (double)nout[0] * nin[0] * nin[2] +
                       (double)nout[0] * nout[2] * nin[2]);
@@ -422,14 +605,16 @@ double KronSum::flops_per_rhs() const {
 }
 
 void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
-                    cudaStream_t s, const Gemm* extra, cudaEvent_t extra_ready, const double* stage0) const {
-  if (extra_ready && !par) {  // only the parity path defers the wait to the kernel that reads the extra term
+                    cudaStream_t s, const Gemm* extra, cudaEvent_t extra_ready, const double* stage0,
+                    const ModeTerms* modes) const {
+  GPFVM_CHECK(!modes || par3, GPFVM_ERR_STATE, "mode terms need the 3D parity-split plan");
+  if (extra_ready && !par && !par3) {  // only the parity path defers the wait to the kernel that reads the extra term
     GPFVM_CUDA(cudaStreamWaitEvent(s, extra_ready, 0));
     extra_ready = nullptr;
   }
   if (extra && extra->K2 > 0 && !(d == 2 && !rev && P > 0)) {
     // not fusable here: the Kronecker sum, then the low-rank term as its own GEMM
-    apply(x, ldx, y, ldy, R, beta, w0, w1, s, nullptr, nullptr, stage0);
+    apply(x, ldx, y, ldy, R, beta, w0, w1, s, nullptr, nullptr, stage0, modes);
     Gemm e;
     e.M = d == 2 ? nout[0] : 1; e.N = nout[d - 1];
     for (int k = 1; k < d - 1; k++) e.M *= nout[k];
@@ -501,6 +686,79 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
     }
     count_launch();
     check_launch("KronSum::apply (parity)");
+    return;
+  }
+  if (par3) {
+    const int64_t n0 = nin[0], n1 = nin[1], n2 = nin[2], h0 = n0 / 2, h1 = n1 / 2, h2 = n2 / 2;
+    const int64_t rest = n1 * n2, n = n0 * rest;
+    // X -> Xt (w1)
+    const int rc = (int)std::max<int64_t>(1, std::min<int64_t>(R, 65535 / h0));
+    for (int r0 = 0; r0 < R; r0 += rc) {
+      const int rn = std::min(rc, R - r0);
+      parity_fwd3_kernel<<<dim3((unsigned)((h2 + 127) / 128), (unsigned)h1, (unsigned)(h0 * rn)), 128, 0, s>>>(
+          x + (int64_t)r0 * ldx, ldx, w1 + (int64_t)r0 * n, n, (int)n0, (int)n1, (int)n2);
+      count_launch();
+    }
+    // stage 0 per group: Z0_g[r][(c0', i')][qg][rest] = H0_(qg, c0) Xt_r[(c0, i)][rest]
+    const int64_t G[2] = {Qs0, Q0 - Qs0};
+    const int64_t zbase[2] = {0, (int64_t)R * n0 * Qs0 * rest};
+    for (int g = 0; g < 2; g++) {
+      if (G[g] == 0) continue;
+      Gemm g0;
+      g0.M = (int)(G[g] * h0); g0.N = (int)rest; g0.K = (int)h0;
+      g0.A = stk[0].ptr + (g ? 2 * Qs0 * h0 * h0 : 0); g0.a_rs = h0; g0.a_cs = 1; g0.a_b1 = 0; g0.a_b2 = G[g] * h0 * h0;
+      g0.B = w1; g0.b_rs = rest; g0.b_cs = 1; g0.b_b1 = n; g0.b_b2 = h0 * rest;
+      g0.C = w0 + zbase[g] + (g ? h0 * G[g] * rest : 0); g0.c_rs = rest; g0.c_cs = 1; g0.c_b1 = n0 * G[g] * rest;
+      g0.c_b2 = (g ? -1 : 1) * h0 * G[g] * rest;
+      g0.batch1 = R; g0.batch2 = 2;
+      run_gemm(g0, s);
+    }
+    // stage 1 per term over the combined (r, j0) batch and the dim-1 class:
+    //   Z1[(r, j0)][(c1', j1')][slot][n2] (+)= c_p H1_(p, c1) Z0[(r, j0)][(c1, k1)][n2]
+    const int64_t z1row = (int64_t)Q2 * n2;
+    std::vector<char> seen(Q2, 0);
+    for (int p = 0; p < P; p++) {
+      const int g = u0[p] >= Qs0, qg = g ? u0[p] - Qs0 : u0[p];
+      Gemm g1;
+      g1.M = (int)h1; g1.N = (int)n2; g1.K = (int)h1;
+      g1.A = stk[1].ptr + (int64_t)p * 2 * h1 * h1; g1.a_rs = h1; g1.a_cs = 1; g1.a_b1 = 0; g1.a_b2 = h1 * h1;
+      g1.B = w0 + zbase[g] + qg * rest; g1.b_rs = n2; g1.b_cs = 1; g1.b_b1 = G[g] * rest; g1.b_b2 = h1 * n2;
+      g1.C = w1 + (int64_t)u2[p] * n2 + (sk1[p] ? h1 * z1row : 0); g1.c_rs = z1row; g1.c_cs = 1; g1.c_b1 = n1 * z1row;
+      g1.c_b2 = (sk1[p] ? -1 : 1) * h1 * z1row;
+      g1.batch1 = (int)(R * n0); g1.batch2 = 2;
+      g1.beta = seen[u2[p]] ? 1.0 : 0.0;
+      seen[u2[p]] = 1;
+      run_gemm(g1, s);
+    }
+    // stage 2 per group of dim-2 factors (K segments over its slots):
+    //   Yt_r[(j0, j1)][(c2', k')] (+)= sum_(slot, k) Z1_r[(j0, j1)][slot][(c2, k)] H2_(slot, c2)[k'][k]
+    bool first = true;
+    for (int g = 0; g < 2; g++) {
+      const int64_t ns = g ? Q2 - Qs2 : Qs2, s0 = g ? Qs2 : 0;
+      if (ns == 0) continue;
+      Gemm g2;
+      g2.M = (int)(n0 * n1); g2.N = (int)h2; g2.K = (int)h2; g2.nseg = (int)ns;
+      g2.A = w1 + s0 * n2; g2.a_rs = z1row; g2.a_cs = 1; g2.a_sg = n2; g2.a_b1 = n0 * n1 * z1row; g2.a_b2 = h2;
+      g2.B = stk[2].ptr + s0 * 2 * h2 * h2; g2.b_rs = 1; g2.b_cs = h2; g2.b_sg = 2 * h2 * h2; g2.b_b1 = 0; g2.b_b2 = h2 * h2;
+      g2.C = w0 + (g ? h2 : 0); g2.c_rs = n2; g2.c_cs = 1; g2.c_b1 = n; g2.c_b2 = (g ? -1 : 1) * h2;
+      g2.batch1 = R; g2.batch2 = 2;
+      g2.beta = first ? 0.0 : 1.0;
+      first = false;
+      run_gemm(g2, s);
+    }
+    if (extra_ready) GPFVM_CUDA(cudaStreamWaitEvent(s, extra_ready, 0));  // mode operands prepared on a side stream
+    for (int r0 = 0; r0 < R; r0 += rc) {
+      const int rn = std::min(rc, R - r0);
+      ModeTerms mt;
+      if (modes) {
+        mt = *modes;
+        for (int e = 0; e < mt.n; e++) mt.m[e].W += (int64_t)r0 * mt.m[e].P * (n / nin[mt.m[e].s]);
+      }
+      parity_inv3_kernel<<<dim3((unsigned)((h2 + 127) / 128), (unsigned)h1, (unsigned)(h0 * rn)), 128, 0, s>>>(
+          w0 + (int64_t)r0 * n, n, y + (int64_t)r0 * ldy, ldy, (int)n0, (int)n1, (int)n2, beta, mt);
+      count_launch();
+    }
+    check_launch("KronSum::apply (3D parity)");
     return;
   }
   if (mid_thin) {

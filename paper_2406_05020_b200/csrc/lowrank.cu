@@ -91,13 +91,22 @@ int64_t ModeUpdate::workspace_per_rhs() const {
   return w;
 }
 
-void ModeUpdate::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta,
-                       const int64_t* block_off, double* w0, double* w1, cudaStream_t st) const {
+void ModeUpdate::prepare(const double* x, int64_t ldx, int R, const int64_t* block_off, double* w0, double* w1,
+                         cudaStream_t st) const {
   const int64_t AB = (int64_t)A * B;
   for (const auto& part : parts)
     for (size_t q = 0; q < part.ks.size(); q++)
       part.ks[q].apply(x + block_off[part.J], ldx, W.ptr + (part.p0 + (int64_t)q) * AB, (int64_t)P * AB, R, 0.0, w0,
                        w1, st);
+}
+
+void ModeUpdate::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta,
+                       const int64_t* block_off, double* w0, double* w1, cudaStream_t st) const {
+  prepare(x, ldx, R, block_off, w0, w1, st);
+  update(y, ldy, R, beta, st);
+}
+
+void ModeUpdate::update(double* y, int64_t ldy, int R, double beta, cudaStream_t st) const {
   const int slab = ns * B;
   const int bx = slab >= 256 ? 256 : 128;
   // ~16 CTAs per SM in total, split between slab chunks (x) and slabs (y)

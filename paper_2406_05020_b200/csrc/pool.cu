@@ -1,4 +1,5 @@
 // Size-bucketed caching device allocator behind DevBuf (see internal.h).
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -28,9 +29,22 @@ size_t round_bytes(size_t b) {
 }
 }  // namespace
 
+// GPFVM_NO_POOL (debugging with compute-sanitizer memcheck): exact-size
+// cudaMalloc / synchronous cudaFree, so an out-of-bounds access leaves its
+// allocation instead of landing in a neighbouring pooled block's padding
+static bool no_pool() {
+  static const bool v = getenv("GPFVM_NO_POOL") != nullptr;
+  return v;
+}
+
 void* pool_alloc(size_t bytes) {
   int dev = 0;
   cudaGetDevice(&dev);
+  if (no_pool()) {
+    void* q = nullptr;
+    GPFVM_CUDA(cudaMalloc(&q, bytes ? bytes : 8));
+    return q;
+  }
   const size_t rb = round_bytes(bytes);
   {
     std::lock_guard<std::mutex> lk(pool().mu);
@@ -54,6 +68,11 @@ void* pool_alloc(size_t bytes) {
 
 void pool_free(void* p, size_t bytes, int dev) {
   if (!p) return;
+  if (no_pool()) {
+    cudaDeviceSynchronize();
+    cudaFree(p);
+    return;
+  }
   if (dev < 0) dev = current_device();
   std::lock_guard<std::mutex> lk(pool().mu);
   pool().free_blocks[{dev, round_bytes(bytes)}].push_back(p);

@@ -92,7 +92,12 @@ int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int m
   // a stationary kernel k(x - y) on one mirror-symmetric site list: the
   // reflection maps cell i to n-1-i and each derivative flips sign, so
   // F[n-1-i][n-1-j] = (-1)^(ml + mr) F[i][j]  (KronSum parity split)
-  if (bl == br && mirror_symmetric(p->blocks[bl].sites[dim])) f.psign = ((ml + mr) & 1) ? -1 : 1;
+  // (two blocks with the same site list, e.g. the PDE rows of a multi-output
+  // system, share the property: the kernel depends on x - y only)
+  const Sites& SL = p->blocks[bl].sites[dim];
+  const Sites& SR = p->blocks[br].sites[dim];
+  const bool same = bl == br || (SL.kind == SR.kind && SL.n == SR.n && SL.lo == SR.lo && SL.hi == SR.hi);
+  if (same && mirror_symmetric(SL)) f.psign = ((ml + mr) & 1) ? -1 : 1;
   p->factors.push_back(std::move(f));
   int id = (int)p->factors.size() - 1;
   p->factor_index[key] = id;
@@ -226,6 +231,12 @@ MatvecPlan::~MatvecPlan() {
   for (auto e : ev) cudaEventDestroy(e);
   for (auto& ff : fused)
     if (ff.ev) cudaEventDestroy(ff.ev);
+  for (auto st : side)
+    if (st) cudaStreamDestroy(st);
+  for (auto e : side_fork)
+    if (e) cudaEventDestroy(e);
+  for (auto e : side_ready)
+    if (e) cudaEventDestroy(e);
   for (auto& lr : lowrank) {
     if (lr.side) cudaStreamDestroy(lr.side);
     if (lr.ev_fork) cudaEventDestroy(lr.ev_fork);
@@ -255,13 +266,14 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
         std::vector<int> sv;
         for (int i = 0; i < p->ndim; i++) {
           f.push_back(p->factors[t.fid[i]].data.ptr);
-          sv.push_back(op.I == op.J ? p->factors[t.fid[i]].psign : 0);
+          sv.push_back(p->factors[t.fid[i]].psign);
         }
         fs.push_back(f);
         sgn.push_back(sv);
       }
       op.ks.build(p->ndim, p->blocks[op.J].shape, p->blocks[op.I].shape, coefs, fs, s, &sgn);
     }
+    refresh_fused_func(*p->plan, s);
     return;
   }
   auto plan = std::make_unique<MatvecPlan>();
@@ -279,7 +291,7 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
         std::vector<int> sv;
         for (int i = 0; i < p->ndim; i++) {
           f.push_back(p->factors[t.fid[i]].data.ptr);
-          sv.push_back(I == J ? p->factors[t.fid[i]].psign : 0);
+          sv.push_back(p->factors[t.fid[i]].psign);
         }
         fs.push_back(f);
         sgn.push_back(sv);
@@ -318,6 +330,15 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
 static int only_branch() {
   static const int only = getenv("GPFVM_TIMING_ONLY_BRANCH") ? atoi(getenv("GPFVM_TIMING_ONLY_BRANCH")) : -1;
   return only;
+}
+
+// the block's mode updates can ride on its own 3D parity-split Kronecker sum
+static bool mode_fusable(const MatvecPlan& pl, int I, const PairOp* diag) {
+  static const bool off = getenv("GPFVM_NO_MODEFUSE") != nullptr;
+  if (off || !diag || !diag->ks.par3) return false;
+  int n = 0;
+  for (const auto& mu : pl.modes[I]) n += mu.P > 0;
+  return n >= 1 && n <= 3;
 }
 
 static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, int nrhs, int64_t ld, cudaStream_t s) {
@@ -364,14 +385,47 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
       overwrite = false;
     }
   }
-  for (const auto& mu : pl.modes[I]) {
-    if (mu.P == 0) continue;
-    mu.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), pl.w0[I].ptr, pl.w1[I].ptr, s);
+  // 3D parity-split diagonal pair: the mode-s updates (IC planes, faces) are
+  // added by its last kernel in the pass that writes y; their operands W are
+  // prepared on a side stream beside the mode products
+  ModeTerms mt;
+  const bool fuse_modes = mode_fusable(pl, I, diag);
+  if (fuse_modes) {
+    if (pl.side.empty()) {
+      pl.side.assign(p->blocks.size(), nullptr);
+      pl.side_fork.assign(p->blocks.size(), nullptr);
+      pl.side_ready.assign(p->blocks.size(), nullptr);
+    }
+    if (!pl.side[I]) {
+      int lo = 0, hi = 0;
+      GPFVM_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      GPFVM_CUDA(cudaStreamCreateWithPriority(&pl.side[I], cudaStreamNonBlocking, lo));
+      GPFVM_CUDA(cudaEventCreateWithFlags(&pl.side_fork[I], cudaEventDisableTiming));
+      GPFVM_CUDA(cudaEventCreateWithFlags(&pl.side_ready[I], cudaEventDisableTiming));
+    }
+    static const bool noside = getenv("GPFVM_MODE_NOSIDE") != nullptr;
+    cudaStream_t ps = noside ? s : pl.side[I];
+    GPFVM_CUDA(cudaEventRecord(pl.side_fork[I], s));
+    GPFVM_CUDA(cudaStreamWaitEvent(pl.side[I], pl.side_fork[I], 0));
+    for (const auto& mu : pl.modes[I]) {
+      if (mu.P == 0) continue;
+      mu.prepare(x, ld, nrhs, pl.block_off.data(), mu.mw0.ptr, mu.mw1.ptr, ps);
+      mt.m[mt.n++] = {mu.U.ptr, mu.W.ptr, mu.P, mu.s};
+    }
+    GPFVM_CUDA(cudaEventRecord(pl.side_ready[I], pl.side[I]));
+    diag->ks.apply(x + B.offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr, pl.w1[I].ptr, s, nullptr,
+                   pl.side_ready[I], nullptr, &mt);
     overwrite = false;
+  } else {
+    for (const auto& mu : pl.modes[I]) {
+      if (mu.P == 0) continue;
+      mu.apply(x, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.block_off.data(), pl.w0[I].ptr, pl.w1[I].ptr, s);
+      overwrite = false;
+    }
   }
   for (int k : pl.by_out[I]) {
     const PairOp& op = pl.pairs[k];
-    if (op.lowrank) continue;
+    if (op.lowrank || (fuse_modes && &op == diag)) continue;
     const double* stage0 = nullptr;
     if (pl.fused_on && pl.fused_of[k] >= 0) {
       const FusedFunc& ff = pl.fused[pl.fused_of[k]];
@@ -393,9 +447,12 @@ static void ensure_plan_workspace(gpfvm_problem* p, int nrhs) {
     for (auto& mu : pl.modes[I]) {
       need = std::max(need, mu.workspace_per_rhs());
       const size_t nw = (size_t)nrhs * std::max(1, mu.P) * mu.A * mu.B;
-      if (mu.W.n < nw) {
+      const size_t nm = (size_t)std::max<int64_t>(1, mu.workspace_per_rhs() * nrhs);
+      if (mu.W.n < nw || mu.mw0.n < nm) {
         pl.release_graphs();
         mu.W.ensure(nw);
+        mu.mw0.ensure(nm);
+        mu.mw1.ensure(nm);
       }
     }
     size_t n = (size_t)std::max<int64_t>(1, need * nrhs);

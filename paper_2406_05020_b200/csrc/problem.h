@@ -36,6 +36,18 @@ struct KronTerm {
   int fid[GPFVM_MAX_DIMS] = {-1, -1, -1, -1};
 };
 
+// Mode-s updates (ModeUpdate below) handed to the 3D parity-split KronSum,
+// whose last kernel adds them while it writes y:
+//   y[i0][i1][i2] += sum_p U_s[i_s][p] W_s[r][p][the other two indices]
+struct ModeTerms {
+  int n = 0;
+  struct T {
+    const double* U;  // [n_s][P]
+    const double* W;  // [R][P][A][B]
+    int P, s;
+  } m[3];
+};
+
 // Fused sum of Kronecker products of one block pair (kron.cu)
 struct KronSum {
   int d = 0, P = 0;
@@ -63,6 +75,11 @@ struct KronSum {
   // parity classes as two-level batched GEMMs: half the flops of every stage
   bool par = false;
   int sg[GPFVM_MAX_DIMS] = {0, 0, 0, 0};
+  // 3D variant (kron.cu): per-term skews, class-batched forward plan; dim-0
+  // and dim-2 factors ordered centrosymmetric first (Qs0 / Qs2 of Q0 / Q2)
+  bool par3 = false;
+  int Qs0 = 0, Qs2 = 0;
+  std::vector<int> sk1;
   // signs (optional): per term, per dimension the factor's psign (0 = none)
   void build(int d, const int* in_shape, const int* out_shape, const std::vector<double>& coefs,
              const std::vector<std::vector<const double*>>& factors, cudaStream_t s,
@@ -78,7 +95,7 @@ struct KronSum {
   // computed elsewhere (FusedFunc) in the layout this plan's stage 0 writes
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, double* w0, double* w1,
              cudaStream_t s, const Gemm* extra = nullptr, cudaEvent_t extra_ready = nullptr,
-             const double* stage0 = nullptr) const;
+             const double* stage0 = nullptr, const ModeTerms* modes = nullptr) const;
 };
 
 // Per-block fast-diagonalisation (bjfd.cu)
@@ -187,8 +204,13 @@ struct ModeUpdate {
   int s = 0, A = 1, ns = 1, B = 1, P = 0;
   DevBuf U;    // [ns][P]
   DevBuf W;    // [R][P][A][B]
+  DevBuf mw0, mw1;  // own workspaces (prepare() on a side stream)
   std::vector<Part> parts;
   int64_t workspace_per_rhs() const;
+  // W for the current input (the small Kronecker products), then the update
+  void prepare(const double* x, int64_t ldx, int R, const int64_t* block_off, double* w0, double* w1,
+               cudaStream_t s) const;
+  void update(double* y, int64_t ldy, int R, double beta, cudaStream_t s) const;
   void apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R, double beta, const int64_t* block_off,
              double* w0, double* w1, cudaStream_t s) const;
 };
@@ -226,6 +248,10 @@ struct MatvecPlan {
   std::vector<int64_t> block_off;
   std::vector<DevBuf> w0, w1;  // per output-block branch
   std::vector<cudaStream_t> branch;
+  // per output block: side stream on which the mode-update operands are
+  // prepared beside the block's own Kronecker sum (created on first use)
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_fork, side_ready;
   cudaStream_t cap = nullptr;
   std::vector<cudaEvent_t> ev;
   struct G {
@@ -279,6 +305,7 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
 void build_plan(gpfvm_problem* p, cudaStream_t s);
 void build_lowrank(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s);
 void build_fused_func(gpfvm_problem* p, MatvecPlan& pl, cudaStream_t s);
+void refresh_fused_func(MatvecPlan& pl, cudaStream_t s);
 double term_flops(const gpfvm_problem* p, const KronTerm& t, const int* in_shape, const int* out_shape);
 int get_factor(gpfvm_problem* p, int out, int dim, int bl, int ml, int br, int mr);
 
