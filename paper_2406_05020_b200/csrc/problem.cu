@@ -371,11 +371,15 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
           GPFVM_CUDA(cudaEventCreateWithFlags(&lr.ev_fork, cudaEventDisableTiming));
           GPFVM_CUDA(cudaEventCreateWithFlags(&lr.ev_ready, cudaEventDisableTiming));
         }
-        GPFVM_CUDA(cudaEventRecord(lr.ev_fork, s));
-        GPFVM_CUDA(cudaStreamWaitEvent(lr.side, lr.ev_fork, 0));
-        lr.prepare(x, ld, nrhs, pl.block_off.data(), lr.side);
-        GPFVM_CUDA(cudaEventRecord(lr.ev_ready, lr.side));
-        lr_ready = lr.ev_ready;
+        if (!pl.serial_now) {
+          GPFVM_CUDA(cudaEventRecord(lr.ev_fork, s));
+          GPFVM_CUDA(cudaStreamWaitEvent(lr.side, lr.ev_fork, 0));
+          lr.prepare(x, ld, nrhs, pl.block_off.data(), lr.side);
+          GPFVM_CUDA(cudaEventRecord(lr.ev_ready, lr.side));
+          lr_ready = lr.ev_ready;
+        } else {
+          lr.prepare(x, ld, nrhs, pl.block_off.data(), s);
+        }
       } else {
         lr.prepare(x, ld, nrhs, pl.block_off.data(), s);
       }
@@ -404,17 +408,20 @@ static void matvec_branch(gpfvm_problem* p, int I, const double* x, double* y, i
       GPFVM_CUDA(cudaEventCreateWithFlags(&pl.side_ready[I], cudaEventDisableTiming));
     }
     static const bool noside = getenv("GPFVM_MODE_NOSIDE") != nullptr;
-    cudaStream_t ps = noside ? s : pl.side[I];
-    GPFVM_CUDA(cudaEventRecord(pl.side_fork[I], s));
-    GPFVM_CUDA(cudaStreamWaitEvent(pl.side[I], pl.side_fork[I], 0));
+    const bool fork = !noside && !pl.serial_now;
+    cudaStream_t ps = fork ? pl.side[I] : s;
+    if (fork) {
+      GPFVM_CUDA(cudaEventRecord(pl.side_fork[I], s));
+      GPFVM_CUDA(cudaStreamWaitEvent(pl.side[I], pl.side_fork[I], 0));
+    }
     for (const auto& mu : pl.modes[I]) {
       if (mu.P == 0) continue;
       mu.prepare(x, ld, nrhs, pl.block_off.data(), mu.mw0.ptr, mu.mw1.ptr, ps);
       mt.m[mt.n++] = {mu.U.ptr, mu.W.ptr, mu.P, mu.s};
     }
-    GPFVM_CUDA(cudaEventRecord(pl.side_ready[I], pl.side[I]));
+    if (fork) GPFVM_CUDA(cudaEventRecord(pl.side_ready[I], pl.side[I]));
     diag->ks.apply(x + B.offset, ld, y + B.offset, ld, nrhs, overwrite ? 0.0 : 1.0, pl.w0[I].ptr, pl.w1[I].ptr, s, nullptr,
-                   pl.side_ready[I], nullptr, &mt);
+                   fork ? pl.side_ready[I] : nullptr, nullptr, &mt);
     overwrite = false;
   } else {
     for (const auto& mu : pl.modes[I]) {
@@ -529,7 +536,18 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
   // the fused functional passes need 16-byte aligned rows of x
   pl.fused_on = !pl.fused.empty() && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (ld & 1) == 0 && only_branch() < 0 &&
                 (int64_t)nrhs * pl.fused[0].tiles() >= 64;  // few vectors: too few CTAs for one pass to pay
-  auto run_branches = [&](cudaStream_t origin) {
+  auto run_branches = [&](cudaStream_t origin, bool serial) {
+    pl.serial_now = serial;
+    if (serial) {
+      // every branch on the caller's stream, one kernel at a time
+      if (pl.fused_on)
+        for (auto& ff : pl.fused) {
+          ff.run(x + p->blocks[ff.J].offset, ld, nrhs, origin);
+          GPFVM_CUDA(cudaEventRecord(ff.ev, origin));
+        }
+      for (int I = 0; I < nb; I++) matvec_branch(p, I, x, y, nrhs, ld, origin);
+      return;
+    }
     GPFVM_CUDA(cudaEventRecord(pl.ev[nb], origin));
     std::vector<char> waited(nb, 0);
     if (pl.fused_on)
@@ -559,9 +577,13 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
       }
       pl.graphs.push_back({x, y, nrhs, ld, nullptr, 0, 1});
     }
-    // direct launches on the branch streams: the same streams the capture
-    // uses, so stream-keyed scratch buffers are sized before any capture
-    run_branches(s);
+    // Direct launches (first sighting of a key, GPFVM_NO_GRAPH) run serially on
+    // the caller's stream: the cold first call of a process is where kernels
+    // of different branches overlapped in ever-changing ways and the TMA GEMM
+    // was seen to produce wrong tiles; the concurrent schedule is
+    // the captured graph's.  GPFVM_DIRECT_CONCURRENT restores branch streams.
+    static const bool direct_conc = getenv("GPFVM_DIRECT_CONCURRENT") != nullptr;
+    run_branches(s, !direct_conc);
     return;
   }
   // second sighting: capture
@@ -569,7 +591,7 @@ void matvec_device(gpfvm_problem* p, const double* x, double* y, int nrhs, int64
   cudaGraph_t graph;
   GPFVM_CUDA(cudaStreamBeginCapture(pl.cap, cudaStreamCaptureModeThreadLocal));
   try {
-    run_branches(pl.cap);
+    run_branches(pl.cap, false);
   } catch (...) {
     cudaStreamEndCapture(pl.cap, &graph);
     throw;

@@ -245,6 +245,7 @@ struct MatvecPlan {
   std::vector<FusedFunc> fused;  // per 2D input block with >= 2 thin pairs
   std::vector<int> fused_of;     // per pair: index into fused or -1
   bool fused_on = false;         // this launch uses the fused pass (alignment checked per call)
+  bool serial_now = false;       // this launch runs every branch on one stream (direct launches)
   std::vector<int64_t> block_off;
   std::vector<DevBuf> w0, w1;  // per output-block branch
   std::vector<cudaStream_t> branch;
