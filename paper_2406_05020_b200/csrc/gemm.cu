@@ -492,6 +492,8 @@ void launch_dmma(const Gemm& g, cudaStream_t s) {
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
     GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (getenv("GPFVM_CARVEOUT"))
+      GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(getenv("GPFVM_CARVEOUT"))));
     configured_dev = dev;
   }
   int64_t nb = (int64_t)g.batch1 * g.batch2 * g.batch3;

@@ -112,7 +112,11 @@ struct TmaSmem {
   // small tiles with 2-3 CTAs per SM) produced partially wrong tiles,
   // nondeterministically (found on config 4 / config 2; never
   // with one launch at a time, never with one CTA per SM).
+#ifdef GPFVM_TMA_SHARED_SMS  // tools/gemm_race.cu: the failing configuration (several CTAs per SM)
+  static constexpr size_t bytes = raw_bytes;
+#else
   static constexpr size_t bytes = raw_bytes > 117 * 1024 ? raw_bytes : 117 * 1024;
+#endif
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool BROW, int MINB>
@@ -247,6 +251,13 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, MINB)
 #pragma unroll
           for (int j = 0; j < TN; j++) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
+      // The fragment loads above are generic-proxy reads of the stage; the TMA
+      // refill is an async-proxy write.  The mbarrier release alone does not
+      // order accesses across the two proxies: without this fence the refill
+      // could land before a queued fragment load had read the old tile (whole
+      // warp tiles wrong, only under shared-memory pressure from co-resident
+      // CTAs, tools/gemm_race.cu).
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -332,6 +343,8 @@ void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
     GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    if (getenv("GPFVM_CARVEOUT_TMA"))
+      GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(getenv("GPFVM_CARVEOUT_TMA"))));
     configured_dev = dev;
   }
   static int sms = 0, per_sm = 0;
@@ -363,6 +376,13 @@ using V2 = TileCfg<128, 64, 2, 2, 4, 1>;   // 64x32 warp tiles, 4 consumer warps
 using V3 = TileCfg<128, 128, 2, 4, 4, 1>;  // 64x32 warp tiles
 using V4 = TileCfg<128, 128, 4, 2, 4, 1>;  // 32x64 warp tiles
 using V5 = TileCfg<256, 64, 4, 2, 3, 1>;   // 64x32 warp tiles
+
+#ifdef GPFVM_TMA_SHARED_SMS  // extra shapes for tools/gemm_race.cu
+using V6 = TileCfg<64, 64, 2, 2, 4, 2>;    // round-2 start: 32x32 warp tiles, 4 stages
+using V7 = TileCfg<64, 64, 4, 2, 4, 1>;    // V1 with 4 stages
+using V8 = TileCfg<64, 64, 2, 2, 6, 2>;    // 32x32 warp tiles, 6 stages
+using V9 = TileCfg<128, 64, 2, 2, 4, 2>;   // V2 with launch bounds for 2 CTAs per SM
+#endif
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool ev(int64_t v) { return (v & 1) == 0; }
@@ -432,6 +452,12 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
     case 3: return run(V3{});
     case 4: return run(V4{});
     case 5: return run(V5{});
+#ifdef GPFVM_TMA_SHARED_SMS
+    case 6: return run(V6{});
+    case 7: return run(V7{});
+    case 8: return run(V8{});
+    case 9: return run(V9{});
+#endif
     default: break;
   }
   // Tile choice: estimated time = waves x tile work / relative DMMA efficiency

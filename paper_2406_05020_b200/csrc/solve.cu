@@ -53,6 +53,30 @@ __global__ void dinv_kernel(double* D, const double* __restrict__ lam, const dou
   D[idx] = 1.0 / d;
 }
 
+// Dense expansion of one Kronecker term of a Gram block (Eq. 20):
+//   S[(c) * ld + r] += coef * prod_i F_i[r_i][c_i],  r / c the row-major
+// multi-indices of the output / input block (S holds G_{I,J}[r][c] at row c,
+// column r; G_bb is symmetric).  One thread per entry.
+struct KronDenseArgs {
+  int d;
+  int nr[GPFVM_MAX_DIMS], nc[GPFVM_MAX_DIMS];
+  const double* F[GPFVM_MAX_DIMS];
+};
+__global__ void kron_dense_kernel(double* S, int64_t ld, KronDenseArgs a, int64_t R, int64_t Cn, double coef) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < R * Cn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / R, r = e - c * R;
+    int64_t rr = r, cc = c;
+    double v = coef;
+    for (int i = a.d - 1; i >= 0; i--) {
+      const int ri = (int)(rr % a.nr[i]), ci = (int)(cc % a.nc[i]);
+      rr /= a.nr[i];
+      cc /= a.nc[i];
+      v *= a.F[i][(int64_t)ri * a.nc[i] + ci];
+    }
+    S[c * ld + r] += v;
+  }
+}
+
 __global__ void set_identity_kernel(double* X, int n, int64_t ld) {
   // X: n vectors of length n at stride ld
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -413,28 +437,33 @@ static void build_ldl(gpfvm_problem* p, Precond& pc, cudaStream_t s) {
   DevBuf S, S0, eye, Lf;
   PhaseTimer pt(s);
   build_rot(p, pc, s);
+  pt.mark("ldl: rotated couplings");
   if (!pc.structured) pc.YT.ensure((size_t)nb * np);
   S.ensure((size_t)nb * nb);
   fill(S.ptr, 0.0, (int64_t)nb * nb, s);
-  // identity right-hand sides per deflated block, pushed through the Kronecker terms
+  // G_bb entry by entry from its Kronecker terms (the deflated blocks are small:
+  // one kernel per term instead of identity blocks pushed through mode products)
   for (size_t jb = 0; jb < pc.bblocks.size(); jb++) {
     const int J = pc.bblocks[jb];
-    const int nJ = (int)p->blocks[J].size;
-    eye.ensure((size_t)nJ * nJ);
-    set_identity_kernel<<<g1((int64_t)nJ * nJ), 256, 0, s>>>(eye.ptr, nJ, nJ);
-    count_launch();
     for (size_t ib = 0; ib < pc.bblocks.size(); ib++) {
       const int I = pc.bblocks[ib];
-      std::vector<const KronTerm*> ts;
-      for (const auto& t : p->terms)
-        if (t.I == I && t.J == J) ts.push_back(&t);
-      if (ts.empty()) continue;
-      // vector c = G_{I,J} e_c -> S row (boff[J]+c), columns boff[I].. (S symmetric)
-      apply_terms(p, p->factors, ts, p->blocks[J].shape, p->blocks[I].shape, eye.ptr, nJ,
-                  S.ptr + pc.boff[jb] * nb + pc.boff[ib], nb, nJ, true, s, p->ws);
+      for (const auto& t : p->terms) {
+        if (t.I != I || t.J != J) continue;
+        KronDenseArgs a;
+        a.d = p->ndim;
+        for (int i = 0; i < p->ndim; i++) {
+          a.nr[i] = p->blocks[I].shape[i];
+          a.nc[i] = p->blocks[J].shape[i];
+          a.F[i] = p->factors[t.fid[i]].data.ptr;
+        }
+        const int64_t Rn = p->blocks[I].size, Cn = p->blocks[J].size;
+        kron_dense_kernel<<<g1(Rn * Cn), 256, 0, s>>>(S.ptr + pc.boff[jb] * nb + pc.boff[ib], nb, a, Rn, Cn, t.coef);
+        count_launch();
+      }
     }
   }
-  pt.mark("ldl: Gbb from identities");
+  check_launch("kron_dense_kernel");
+  pt.mark("ldl: Gbb from its Kronecker terms");
   // noise on the diagonal of G_bb
   {
     std::vector<double> nz(nb);

@@ -32,6 +32,21 @@ static double* dalloc(int64_t n, unsigned seed) {
   return p;
 }
 
+// mode 3: a kernel with the cp.async GEMM's footprint (128 threads, 38 KB of
+// dynamic shared memory, 288 CTAs) that never issues cp.async
+__global__ void dummy_smem_kernel(const double* __restrict__ in, double* out, int n) {
+  extern __shared__ double sm[];
+  const int words = 38912 / 8;
+  double acc = 0.0;
+  for (int it = 0; it < 40; it++) {
+    for (int i = threadIdx.x; i < words; i += blockDim.x) sm[i] = in[(blockIdx.x * 977 + i + it * 131) % n];
+    __syncthreads();
+    for (int i = threadIdx.x; i < words; i += blockDim.x) acc += sm[(i * 7 + it) % words];
+    __syncthreads();
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main(int argc, char** argv) {
   const int mode = argc > 1 ? atoi(argv[1]) : 0, reps = argc > 2 ? atoi(argv[2]) : 200;
   cudaStream_t sa, sb;
@@ -66,7 +81,8 @@ int main(int argc, char** argv) {
   for (int r = 0; r < reps; r++) {
     cudaMemsetAsync(Ca, 0, csz * 8, sa);
     for (int q = 0; q < 6; q++) {
-      if (mode != 2) run_gemm(b, sb);
+      if (mode == 3) dummy_smem_kernel<<<288, 128, 38912, sb>>>(b.A, b.C, 8 * 192 * 191);
+      else if (mode != 2) run_gemm(b, sb);
       if (q == 2) try_tma_gemm(a, sa);
     }
     cudaStreamSynchronize(sa);
