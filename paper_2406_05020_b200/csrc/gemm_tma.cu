@@ -106,17 +106,16 @@ struct TmaSmem {
   static constexpr int A_BYTES = BM * 128;  // [BM][16] doubles
   static constexpr int B_BYTES = BN * 128;  // [BN][16] or [BN/16][16][16]
   static constexpr size_t raw_bytes = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 2 * STAGES * sizeof(uint64_t);
-  // At least 117 KB (more than half of the SM's 227 KB): at most ONE CTA of
-  // any variant of this kernel is resident per SM.  CTAs of two different
-  // launches of the kernel sharing an SM (concurrent streams / graph branches,
-  // small tiles with 2-3 CTAs per SM) produced partially wrong tiles,
-  // nondeterministically (found on config 4 / config 2; never
-  // with one launch at a time, never with one CTA per SM).
-#ifdef GPFVM_TMA_SHARED_SMS  // tools/gemm_race.cu: the failing configuration (several CTAs per SM)
-  static constexpr size_t bytes = raw_bytes;
-#else
-  static constexpr size_t bytes = raw_bytes > 117 * 1024 ? raw_bytes : 117 * 1024;
-#endif
+  // Shared memory asked for at launch: the ring, or at least `floor_kb` KB.  A
+  // floor above half of the SM's 227 KB keeps ONE CTA of this kernel per SM;
+  // that was the first mitigation of the wrong-tile failure of DESIGN.md 4.4,
+  // whose root cause (a missing fence.proxy.async, fixed in the consumer loop)
+  // does not need it.  GPFVM_TMA_SMEM_FLOOR_KB sets it (default 0: the small
+  // tile variants run 2 CTAs per SM).
+  static size_t bytes_at_launch() {
+    static const size_t floor_kb = getenv("GPFVM_TMA_SMEM_FLOOR_KB") ? (size_t)atoi(getenv("GPFVM_TMA_SMEM_FLOOR_KB")) : 0;
+    return std::max(raw_bytes, floor_kb * 1024);
+  }
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES, bool BROW, int MINB>
@@ -342,7 +341,7 @@ void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   int dev = 0;
   cudaGetDevice(&dev);
   if (configured_dev != dev) {
-    GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes));
+    GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes_at_launch()));
     if (getenv("GPFVM_CARVEOUT_TMA"))
       GPFVM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(getenv("GPFVM_CARVEOUT_TMA"))));
     configured_dev = dev;
@@ -350,7 +349,7 @@ void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   static int sms = 0, per_sm = 0;
   if (sms == 0) {
     GPFVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GPFVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (WARPS_M * WARPS_N + 1) * 32, L::bytes));
+    GPFVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (WARPS_M * WARPS_N + 1) * 32, L::bytes_at_launch()));
     per_sm = std::max(per_sm, 1);
   }
   const int64_t tiles = (int64_t)((a.N + BN - 1) / BN) * ((a.M + BM - 1) / BM) * batch;
@@ -359,7 +358,7 @@ void launch_tma(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   // IC/BC branches of the matvec graph interleave at CTA granularity
   static const bool nonpersist = getenv("GPFVM_TMA_NONPERSIST") != nullptr;
   const int grid = nonpersist ? (int)std::min<int64_t>(tiles, 1 << 30) : (int)std::min<int64_t>(tiles, (int64_t)sms * per_sm);
-  kern<<<grid, (WARPS_M * WARPS_N + 1) * 32, L::bytes, s>>>(ma, mb, ma2, mb2, a);
+  kern<<<grid, (WARPS_M * WARPS_N + 1) * 32, L::bytes_at_launch(), s>>>(ma, mb, ma2, mb2, a);
   count_launch();
   check_launch("dgemm_tma_kernel");
 }
@@ -467,14 +466,13 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
     const int64_t tiles = ((g.M + bm - 1) / bm) * (int64_t)((g.N + bn - 1) / bn) * batch;
     return (double)((tiles + 147) / 148) * bm * bn / eff;
   };
-  // Every eligible GEMM runs here, however small its grid.  Routing the small
-  // IC/BC coupling GEMMs to the cp.async kernel (more, smaller CTAs) was
-  // slightly faster on config 2 but made this kernel's results
-  // nondeterministically wrong when CTAs of the two kernels shared SMs on
-  // concurrent streams (config 4: 23 of 40 matvecs had wrong tiles; with every
-  // GEMM on this kernel 0 of 110).  GPFVM_TMA_MIN_TILES restores
-  // the threshold for experiments.
-  static const int min_tiles = getenv("GPFVM_TMA_MIN_TILES") ? atoi(getenv("GPFVM_TMA_MIN_TILES")) : 0;
+  // grids that cannot fill the machine even with 64x64 tiles go to the
+  // cp.async kernel's 32x32 tiles (more CTAs; these are the short IC/BC
+  // coupling GEMMs that run concurrently with the PDE branch; config 2:
+  // 0.68 -> 0.62 ms).  While the consumer loop lacked its proxy fence this
+  // mix was what exposed the wrong tiles; GPFVM_TMA_MIN_TILES=0
+  // sends every eligible GEMM here.
+  static const int min_tiles = getenv("GPFVM_TMA_MIN_TILES") ? atoi(getenv("GPFVM_TMA_MIN_TILES")) : 148;
   if (((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * batch < min_tiles) return false;
   const double c4 = cost(128, 128, 1.0), c0 = cost(128, 64, 0.92), c1 = cost(64, 64, 0.8);
   if (c4 <= c0 && c4 <= c1) return run(V4{});

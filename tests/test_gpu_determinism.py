@@ -2,9 +2,11 @@
 (one branch per output block plus the side streams that prepare the coupling
 operands): every reduction in the path has a fixed order, so repeated calls
 must agree bit for bit, and the first must agree with the oracle.  Guards the
-class of failure found in round 2: CTAs of the TMA GEMM sharing
-SMs with CTAs of the cp.async GEMM on concurrent streams produced wrong tiles
-in about half of the config-4 matvecs, never in the same place twice."""
+failure found in round 2: the TMA GEMM's consumer warps
+released a pipeline stage without a fence.proxy.async between their
+generic-proxy reads and the TMA refill, and under shared-memory pressure from
+co-resident CTAs about half of the config-4 matvecs had wrong warp tiles,
+never in the same place twice."""
 import numpy as np
 import pytest
 
