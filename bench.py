@@ -201,6 +201,7 @@ def bench_config(builder, R, dev, peak, traffic, world, solve_budget=0, full_reo
     out = {"workload": p.name if hasattr(p, "name") else builder.__name__, "n_obs": int(N), "nrhs": R, "matvec_ms": ms,
            "GB_s": world * 16.0 * N * R / (ms * 1e-3) / 1e9, "TFLOP_s": flops / (ms * 1e-3) / 1e12,
            "frac": flops / (ms * 1e-3) / 1e12 / peak, "algorithmic_bytes": 16 * N * R,
+           "unsplit_plan_equivalent_tflops": gp.matvec_flops_unsplit() * R / (ms * 1e-3) / 1e12,
            "traffic": traffic.get("dram_bytes"), "traffic_source": traffic.get("source")}
     if solve_budget > 0:
         # the paper's fixed IterGP budget for its 3D problem (P:l.444: 1250
@@ -459,7 +460,11 @@ def main():
                 "peak_source": peak_src,
                 "traffic": traffic.get("config1", {}).get("dram_bytes"),
                 "traffic_source": traffic.get("config1", {}).get("source"),
-                "algorithmic_bytes": bytes_mv, "flops_per_launch": flops_mv}
+                "algorithmic_bytes": bytes_mv, "flops_per_launch": flops_mv,
+                # context: the same matvec through the unsplit plan would execute these flops
+                # (the reflection-parity split halves the PDE-PDE pairs)
+                "flops_per_launch_unsplit_plan": gp.matvec_flops_unsplit() * R,
+                "unsplit_plan_equivalent_tflops": gp.matvec_flops_unsplit() * R / (mv_ms_max * 1e-3) / 1e12}
     configs = None
     if not args.no_configs:
         configs = {}

@@ -352,6 +352,11 @@ int64_t gpfvm_launch_count(void);
  * term cancellation of DESIGN.md R6; low-rank and mode updates counted as
  * the GEMMs/streams actually run).  0 before assembly. */
 double gpfvm_matvec_flops(const gpfvm_problem* p);
+/* The same count for the plan without the reflection-parity split
+ * (a split block pair executes exactly half the flops of its
+ * unsplit plan): context for throughput figures, equal to
+ * gpfvm_matvec_flops where no pair is split. */
+double gpfvm_matvec_flops_unsplit(const gpfvm_problem* p);
 /* FP64 tensor-core peak probe (the roofline denominator bench.py reports):
  * a register-only DMMA.8x8x4 (mma.sync.m8n8k4.f64) kernel, 4 CTAs x 8 warps
  * per SM, each warp issuing 8 independent accumulator chains; best of two

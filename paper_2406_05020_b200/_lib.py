@@ -111,6 +111,7 @@ EXPORTS = {
     "gpfvm_iter_step_final": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gpfvm_launch_count": (C.c_int64, []),
     "gpfvm_matvec_flops": (C.c_double, [C.c_void_p]),
+    "gpfvm_matvec_flops_unsplit": (C.c_double, [C.c_void_p]),
 }
 
 _lib = None

@@ -188,3 +188,6 @@ class GpfvmProblem:
 
     def matvec_flops(self) -> float:
         return float(self.lib.gpfvm_matvec_flops(self.handle))
+
+    def matvec_flops_unsplit(self) -> float:
+        return float(self.lib.gpfvm_matvec_flops_unsplit(self.handle))

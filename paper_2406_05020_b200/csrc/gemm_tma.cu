@@ -371,7 +371,7 @@ struct TileCfg {
 // every variant: 8 consumer warps, one CTA per SM (see TmaSmem::bytes)
 using V0 = TileCfg<128, 64, 4, 2, 6, 1>;   // 32x32 warp tiles
 using V1 = TileCfg<64, 64, 4, 2, 6, 1>;    // 16x32 warp tiles (small grids)
-using V2 = TileCfg<128, 64, 2, 2, 4, 1>;   // 64x32 warp tiles, 4 consumer warps
+using V2 = TileCfg<128, 64, 2, 2, 4, 2>;   // 64x32 warp tiles, 4 consumer warps, 2 CTAs per SM
 using V3 = TileCfg<128, 128, 2, 4, 4, 1>;  // 64x32 warp tiles
 using V4 = TileCfg<128, 128, 4, 2, 4, 1>;  // 32x64 warp tiles
 using V5 = TileCfg<256, 64, 4, 2, 3, 1>;   // 64x32 warp tiles
@@ -474,9 +474,16 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
   // sends every eligible GEMM here.
   static const int min_tiles = getenv("GPFVM_TMA_MIN_TILES") ? atoi(getenv("GPFVM_TMA_MIN_TILES")) : 148;
   if (((g.M + 63) / 64) * (int64_t)((g.N + 63) / 64) * batch < min_tiles) return false;
-  const double c4 = cost(128, 128, 1.0), c0 = cost(128, 64, 0.92), c1 = cost(64, 64, 0.8);
+  // 128x64: 8 warps of 32x32 on one CTA per SM (V0), or 4 warps of 64x32 on two (V2, GPFVM_TMA_MID=2)
+  static const int mid = getenv("GPFVM_TMA_MID") ? atoi(getenv("GPFVM_TMA_MID")) : 0;
+  auto cost2 = [&](int bm, int bn, double eff) {  // two CTAs per SM
+    const int64_t tiles = ((g.M + bm - 1) / bm) * (int64_t)((g.N + bn - 1) / bn) * batch;
+    return (double)((tiles + 295) / 296) * bm * bn * 2 / eff;
+  };
+  const double c4 = cost(128, 128, 1.0), c0 = mid == 2 ? cost2(128, 64, 0.98) : cost(128, 64, 0.92),
+               c1 = cost2(64, 64, 0.8);
   if (c4 <= c0 && c4 <= c1) return run(V4{});
-  if (c0 <= c1) return run(V0{});
+  if (c0 <= c1) return mid == 2 ? run(V2{}) : run(V0{});
   return run(V1{});
 }
 

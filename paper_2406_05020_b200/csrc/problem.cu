@@ -311,8 +311,13 @@ void build_plan(gpfvm_problem* p, cudaStream_t s) {
   build_fused_func(p, *plan, s);
   // executed flops per right-hand side: plain pairs + low-rank / mode updates
   plan->flops_per_rhs = 0.0;
+  plan->flops_split_saved = 0.0;
   for (const auto& op : plan->pairs)
-    if (!op.lowrank) plan->flops_per_rhs += op.ks.flops_per_rhs();
+    if (!op.lowrank) {
+      plan->flops_per_rhs += op.ks.flops_per_rhs();
+      // a parity-split pair executes exactly half the flops of its unsplit plan
+      if (op.ks.par || op.ks.par3) plan->flops_split_saved += op.ks.flops_per_rhs();
+    }
   for (const auto& lr : plan->lowrank) {
     for (const auto& part : lr.parts)
       plan->flops_per_rhs += 2.0 * part.nin * part.P * (part.type == 0 ? lr.n1 : lr.n0);
@@ -799,6 +804,11 @@ int gpfvm_gram_matvec(gpfvm_problem* p, const double* x, double* y, int nrhs, in
       GPFVM_CUDA(cudaStreamSynchronize(s));
     }
   });
+}
+
+double gpfvm_matvec_flops_unsplit(const gpfvm_problem* p) {
+  if (!p) return 0.0;
+  return gpfvm_matvec_flops(p) + (p->plan ? p->plan->flops_split_saved : 0.0);
 }
 
 double gpfvm_matvec_flops(const gpfvm_problem* p) {

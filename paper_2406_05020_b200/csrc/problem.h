@@ -266,6 +266,7 @@ struct MatvecPlan {
   };
   std::vector<G> graphs;
   double flops_per_rhs = 0.0;
+  double flops_split_saved = 0.0;  // flops the reflection-parity split removed (context for the roofline)
   ~MatvecPlan();
   void release_graphs();
 };
