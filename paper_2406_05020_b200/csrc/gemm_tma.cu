@@ -375,6 +375,11 @@ using V2 = TileCfg<128, 64, 2, 2, 4, 2>;   // 64x32 warp tiles, 4 consumer warps
 using V3 = TileCfg<128, 128, 2, 4, 4, 1>;  // 64x32 warp tiles
 using V4 = TileCfg<128, 128, 4, 2, 4, 1>;  // 32x64 warp tiles
 using V5 = TileCfg<256, 64, 4, 2, 3, 1>;   // 64x32 warp tiles
+// 96-wide tiles for the half sizes of 192-cell dimensions (config 4 after the
+// parity split: M or N = 96 wastes a quarter of a 128-wide tile)
+using W0 = TileCfg<96, 192, 3, 4, 4, 1>;   // 32x48 warp tiles, 12 consumer warps: one M = 96, N = 192 batch entry per tile
+using W1 = TileCfg<128, 96, 4, 2, 4, 1>;   // 32x48 warp tiles
+using W2 = TileCfg<96, 128, 3, 4, 4, 1>;   // 32x32 warp tiles, 12 consumer warps
 
 #ifdef GPFVM_TMA_SHARED_SMS  // extra shapes for tools/gemm_race.cu
 using V6 = TileCfg<64, 64, 2, 2, 4, 2>;    // round-2 start: 32x32 warp tiles, 4 stages
@@ -451,6 +456,9 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
     case 3: return run(V3{});
     case 4: return run(V4{});
     case 5: return run(V5{});
+    case 10: return run(W0{});
+    case 11: return run(W1{});
+    case 12: return run(W2{});
 #ifdef GPFVM_TMA_SHARED_SMS
     case 6: return run(V6{});
     case 7: return run(V7{});
@@ -482,8 +490,19 @@ static bool try_tma_gemm_impl(const Gemm& g, cudaStream_t s) {
   };
   const double c4 = cost(128, 128, 1.0), c0 = mid == 2 ? cost2(128, 64, 0.98) : cost(128, 64, 0.92),
                c1 = cost2(64, 64, 0.8);
-  if (c4 <= c0 && c4 <= c1) return run(V4{});
-  if (c0 <= c1) return mid == 2 ? run(V2{}) : run(V0{});
+  // 96-wide tiles only where a dimension is a multiple of 96 but not of 128
+  // (they exist for the half sizes of 192-cell dimensions)
+  static const bool no96 = getenv("GPFVM_TMA_NO96") != nullptr;
+  const bool m96 = !no96 && g.M % 96 == 0 && g.M % 128 != 0, n96 = !no96 && g.N % 96 == 0 && g.N % 128 != 0;
+  const double big = 1e300;
+  const double w0 = (m96 && g.N % 192 == 0) ? cost(96, 192, 0.95) : big, w1 = n96 ? cost(128, 96, 0.97) : big,
+               w2 = m96 ? cost(96, 128, 0.93) : big;
+  const double best = std::min(std::min(std::min(c4, c0), std::min(c1, w0)), std::min(w1, w2));
+  if (best == w0) return run(W0{});
+  if (best == w1) return run(W1{});
+  if (best == w2) return run(W2{});
+  if (best == c4) return run(V4{});
+  if (best == c0) return mid == 2 ? run(V2{}) : run(V0{});
   return run(V1{});
 }
 
