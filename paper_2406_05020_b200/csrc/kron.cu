@@ -304,6 +304,101 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Vectorised variant of parity_inv3_kernel: two consecutive k per thread
+// (16-byte loads and stores; the mirrored pair n2-1-k, n2-2-k is one reversed
+// double2), so every W / U value fetched serves four outputs.  Needs 16-byte
+// aligned y, yt, W and even leading dimensions (checked by the caller).
+__global__ void __launch_bounds__(128)
+    parity_inv3v_kernel(const double* __restrict__ yt, int64_t ldt, double* __restrict__ y, int64_t ldy, int n0, int n1,
+                        int n2, double beta, ModeTerms mt) {
+  const int h0 = n0 >> 1, h1 = n1 >> 1, h2 = n2 >> 1;
+  const int k = 2 * (blockIdx.x * blockDim.x + threadIdx.x), j = blockIdx.y;
+  const int i = blockIdx.z % h0, r = blockIdx.z / h0;
+  if (k >= h2) return;
+  const double* tr = yt + (int64_t)r * ldt;
+  double2 v[8];
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    const int ii = ((m & 4) ? h0 : 0) + i, jj = ((m & 2) ? h1 : 0) + j, kk = ((m & 1) ? h2 : 0) + k;
+    v[m] = *reinterpret_cast<const double2*>(tr + ((int64_t)ii * n1 + jj) * n2 + kk);
+  }
+#pragma unroll
+  for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+    for (int m = 0; m < 8; m++)
+      if (!(m & bit)) {
+        const double2 a = v[m], b = v[m | bit];
+        v[m] = make_double2(a.x + b.x, a.y + b.y);
+        v[m | bit] = make_double2(a.x - b.x, a.y - b.y);
+      }
+  // v[m].x belongs to k (mirror n2-1-k), v[m].y to k+1 (mirror n2-2-k)
+#pragma unroll
+  for (int m = 0; m < 8; m++) { v[m].x *= 0.125; v[m].y *= 0.125; }
+  const int I2[2] = {i, n0 - 1 - i}, J2[2] = {j, n1 - 1 - j};
+  const int km = n2 - 2 - k;  // mirrored pair starts here: (km, km+1) mirror (k+1, k)
+  for (int e = 0; e < mt.n; e++) {
+    const int P = mt.m[e].P, sd = mt.m[e].s;
+    const double* U = mt.m[e].U;
+    if (sd == 2) {
+      // y[i][j][k] += U[k][p] W[p][i][j]: W broadcast over the lanes, U per k
+      const int64_t AB = (int64_t)n0 * n1;
+      const double* W = mt.m[e].W + (int64_t)r * P * AB;
+      for (int p = 0; p < P; p++) {
+        const double ua = U[(int64_t)k * P + p], ub = U[(int64_t)(k + 1) * P + p];
+        const double uc = U[(int64_t)(km + 1) * P + p], ud = U[(int64_t)km * P + p];  // mirrors of k, k+1
+        const double* Wp = W + (int64_t)p * AB;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {  // q = (mi, mj)
+          const double w = Wp[(int64_t)I2[q >> 1] * n1 + J2[q & 1]];
+          v[2 * q].x = fma(ua, w, v[2 * q].x);
+          v[2 * q].y = fma(ub, w, v[2 * q].y);
+          v[2 * q + 1].x = fma(uc, w, v[2 * q + 1].x);
+          v[2 * q + 1].y = fma(ud, w, v[2 * q + 1].y);
+        }
+      }
+    } else {
+      // sd == 0: y[i][j][k] += U[i][p] W[p][j][k];  sd == 1: y[i][j][k] += U[j][p] W[p][i][k]
+      const int64_t AB = (sd == 0 ? (int64_t)n1 : (int64_t)n0) * n2;
+      const double* W = mt.m[e].W + (int64_t)r * P * AB;
+      const int a0 = sd == 0 ? I2[0] : J2[0], a1 = sd == 0 ? I2[1] : J2[1];
+      const int b0 = sd == 0 ? J2[0] : I2[0], b1 = sd == 0 ? J2[1] : I2[1];
+      for (int p = 0; p < P; p++) {
+        const double u0 = U[(int64_t)a0 * P + p], u1 = U[(int64_t)a1 * P + p];
+        const double* Wp = W + (int64_t)p * AB;
+        const double2 w00 = *reinterpret_cast<const double2*>(Wp + (int64_t)b0 * n2 + k);
+        const double2 w01 = *reinterpret_cast<const double2*>(Wp + (int64_t)b0 * n2 + km);  // (.y, .x) mirror (k, k+1)
+        const double2 w10 = *reinterpret_cast<const double2*>(Wp + (int64_t)b1 * n2 + k);
+        const double2 w11 = *reinterpret_cast<const double2*>(Wp + (int64_t)b1 * n2 + km);
+        // output m = (mi, mj, mk); the W row index b follows mj (sd == 0) or mi (sd == 1),
+        // the U index a follows mi (sd == 0) or mj (sd == 1)
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+          const int mi = m >> 2, mj = (m >> 1) & 1, mk = m & 1;
+          const double u = (sd == 0 ? mi : mj) ? u1 : u0;
+          const bool brow1 = (sd == 0 ? mj : mi) != 0;
+          const double2 w = brow1 ? (mk ? w11 : w10) : (mk ? w01 : w00);
+          // mk = 0: (.x, .y) are k, k+1; mk = 1: the mirrored pair, stored reversed
+          v[m].x = fma(u, mk ? w.y : w.x, v[m].x);
+          v[m].y = fma(u, mk ? w.x : w.y, v[m].y);
+        }
+      }
+    }
+  }
+  double* yr = y + (int64_t)r * ldy;
+#pragma unroll
+  for (int m = 0; m < 8; m++) {
+    const int64_t row = ((int64_t)I2[m >> 2] * n1 + J2[(m >> 1) & 1]) * n2;
+    double2* yp = reinterpret_cast<double2*>(yr + row + ((m & 1) ? km : k));
+    double2 o = (m & 1) ? make_double2(v[m].y, v[m].x) : v[m];
+    if (beta != 0.0) {
+      const double2 old = *yp;
+      o.x = fma(beta, old.x, o.x);
+      o.y = fma(beta, old.y, o.y);
+    }
+    *yp = o;
+  }
+}
+
 double order_flops(int d, int P, const int* nin, const int* nout, bool rev) {
   int cur[GPFVM_MAX_DIMS];
   for (int i = 0; i < d; i++) cur[i] = nin[i];
@@ -754,8 +849,15 @@ void KronSum::apply(const double* x, int64_t ldx, double* y, int64_t ldy, int R,
         mt = *modes;
         for (int e = 0; e < mt.n; e++) mt.m[e].W += (int64_t)r0 * mt.m[e].P * (n / nin[mt.m[e].s]);
       }
-      parity_inv3_kernel<<<dim3((unsigned)((h2 + 127) / 128), (unsigned)h1, (unsigned)(h0 * rn)), 128, 0, s>>>(
-          w0 + (int64_t)r0 * n, n, y + (int64_t)r0 * ldy, ldy, (int)n0, (int)n1, (int)n2, beta, mt);
+      static const bool no_vec = getenv("GPFVM_NO_INV3V") != nullptr;
+      bool vec = !no_vec && ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(w0)) & 15) == 0 && (ldy & 1) == 0;
+      for (int e = 0; e < mt.n; e++) vec = vec && (reinterpret_cast<uintptr_t>(mt.m[e].W) & 15) == 0;
+      if (vec)
+        parity_inv3v_kernel<<<dim3((unsigned)((h2 / 2 + 127) / 128), (unsigned)h1, (unsigned)(h0 * rn)), 128, 0, s>>>(
+            w0 + (int64_t)r0 * n, n, y + (int64_t)r0 * ldy, ldy, (int)n0, (int)n1, (int)n2, beta, mt);
+      else
+        parity_inv3_kernel<<<dim3((unsigned)((h2 + 127) / 128), (unsigned)h1, (unsigned)(h0 * rn)), 128, 0, s>>>(
+            w0 + (int64_t)r0 * n, n, y + (int64_t)r0 * ldy, ldy, (int)n0, (int)n1, (int)n2, beta, mt);
       count_launch();
     }
     check_launch("KronSum::apply (3D parity)");
