@@ -36,3 +36,48 @@ def test_matvec_bitwise_repeatable_and_equal_to_oracle(cfg, R, calls):
     for c in range(calls):          # direct launch, graph capture, graph replays
         gp.gpfvm_gram_matvec(xt, out=out)
         assert torch.equal(out, first), f"call {c}: max diff {float((out - first).abs().max())}"
+
+
+def test_tma_gemm_beside_cp_async_gemm_is_repeatable():
+    """The two-stream situation of tools/gemm_race.cu through the C ABI: a TMA
+    GEMM with 64x64 tiles (two CTAs per SM) repeated on one stream while the
+    other stream runs GEMMs the TMA path rejects (odd leading dimension ->
+    cp.async kernel).  Every repetition must equal the solitary result bit for
+    bit (without the proxy fence about a third differed)."""
+    import ctypes as C
+    from paper_2406_05020_b200 import _lib
+    lib = _lib.load()
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device="cpu").manual_seed(5)
+    M, N, K = 64, 64 * 1184, 96                     # one row of 64x64 tiles: the 2-CTA-per-SM variant
+    A = torch.rand(M, K, generator=g, dtype=torch.float64).to(dev) - 0.5
+    B = torch.rand(K, N, generator=g, dtype=torch.float64).to(dev) - 0.5
+    Cm = torch.empty(M, N, dtype=torch.float64, device=dev)
+    m2, k2 = 768, 191                               # odd lda: not TMA-eligible
+    A2 = torch.rand(m2, k2, generator=g, dtype=torch.float64).to(dev)
+    B2 = torch.rand(k2, m2, generator=g, dtype=torch.float64).to(dev)
+    C2 = torch.empty(m2, m2, dtype=torch.float64, device=dev)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    def gemm(m, n, k, a, lda, b, ldb, c, ldc, s):
+        rc = lib.gpfvm_gemm(m, n, k, 1.0, C.c_void_p(a.data_ptr()), lda, C.c_void_p(b.data_ptr()), ldb, 0.0,
+                            C.c_void_p(c.data_ptr()), ldc, C.c_void_p(s.cuda_stream))
+        assert rc == 0, lib.gpfvm_last_error()
+
+    gemm(M, N, K, A, K, B, N, Cm, N, sa)
+    torch.cuda.synchronize()
+    first = Cm.clone()
+    ref = (A.cpu().numpy() @ B.cpu().numpy())
+    assert np.abs(first.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+    bad = 0
+    for rep in range(150):
+        Cm.zero_()
+        torch.cuda.synchronize()
+        for q in range(6):
+            gemm(m2, m2, k2, A2, k2, B2, m2, C2, m2, sb)
+            if q == 2:
+                gemm(M, N, K, A, K, B, N, Cm, N, sa)
+        torch.cuda.synchronize()
+        bad += not torch.equal(Cm, first)
+    assert bad == 0, f"{bad} of 150 repetitions differ from the solitary result"
