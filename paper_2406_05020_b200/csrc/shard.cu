@@ -93,6 +93,7 @@ struct ShardTermIn {
   int I = 0, J = 0;
   double coef = 0.0;
   const double* f[GPFVM_MAX_DIMS] = {nullptr, nullptr, nullptr, nullptr};
+  int sg[GPFVM_MAX_DIMS] = {0, 0, 0, 0};  // reflection parity of each factor (Factor::psign; 0: none)
   int64_t tkey = 0;
 };
 
@@ -140,6 +141,7 @@ struct ShardOp {
     int J = 0;
     std::vector<double> coefs;                     // terms of the pair (I, J) in this group
     std::vector<std::vector<const double*>> fs;    // their spatial factors (dims 1..d-1)
+    std::vector<std::vector<int>> sgn;             // and the factors' reflection parities (KronSum parity split)
     KronSum ks;  // spatial (d-1)-dim Kronecker sum J -> I (coefficients folded)
   };
   struct Group {
@@ -211,6 +213,7 @@ void ShardOp::plan(const ShardLayout& lay, const std::vector<ShardTermIn>& terms
     for (const ShardTermIn* t : kv.second) {
       m.coefs.push_back(t->coef);
       m.fs.push_back(std::vector<const double*>(t->f + 1, t->f + d));
+      m.sgn.push_back(std::vector<int>(t->sg + 1, t->sg + d));
     }
     G.mem.push_back(std::move(m));
   }
@@ -314,7 +317,7 @@ void ShardOp::materialize(const gpfvm_problem* p, cudaStream_t s) {
   const int me = L.rank, nb = L.nb, d = L.d;
   for (auto& G : groups)
     for (auto& m : G.mem) {
-      m.ks.build(d - 1, p->blocks[m.J].shape + 1, p->blocks[G.I].shape + 1, m.coefs, m.fs, s);
+      m.ks.build(d - 1, p->blocks[m.J].shape + 1, p->blocks[G.I].shape + 1, m.coefs, m.fs, s, &m.sgn);
       wsz = std::max<int64_t>(wsz, m.ks.workspace_per_rhs() * std::max(1, L.rows(m.J, me)));
     }
   Zall.ensure((size_t)std::max<int64_t>(1, zsz));
@@ -476,7 +479,10 @@ std::vector<ShardTermIn> gram_shard_terms(const gpfvm_problem* p) {
     st.I = t.I;
     st.J = t.J;
     st.coef = t.coef;
-    for (int i = 0; i < p->ndim; i++) st.f[i] = p->factors[t.fid[i]].data.ptr;
+    for (int i = 0; i < p->ndim; i++) {
+      st.f[i] = p->factors[t.fid[i]].data.ptr;
+      st.sg[i] = p->factors[t.fid[i]].psign;
+    }
     auto key = fid_key.at(t.fid[0]);
     auto it = tk.find(key);
     st.tkey = (it == tk.end()) ? (tk[key] = (int64_t)tk.size()) : it->second;
