@@ -455,7 +455,7 @@ def main():
     fp64_peak, peak_src = fp64_peak_live(gp)
     traffic = _traffic()
     achieved = flops_mv / (mv_ms_max * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs, whole matvec graph)",
+    roofline = {"bound": "tensor", "kernel": "gpfvm_gram_matvec (DMMA FP64 mode-product GEMMs of the reflection-parity-split plan, whole matvec graph; achieved = executed flops / time)",
                 "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
                 "peak_source": peak_src,
                 "traffic": traffic.get("config1", {}).get("dram_bytes"),
